@@ -1,0 +1,114 @@
+// qfs_chain.cuh -- stage 4: iterated mod-p matrix-vector chain with per-surface early exit.
+//
+// Replaces the loop of height_matrix (height.py:135-144) around matvec (modmatrix.py:109-131):
+//     for h = 2..bound:  v <- M v (mod p);  iterations += 1;  if v[cap] != 0: height = h, stop.
+// The reference accumulates uint64 products in column blocks of 2048 and reduces per block; any
+// reduction cadence inside the overflow budget is bit-identical (modmatrix.py:35-49).  Here a row
+// dot product is at most N (p-1)^2 <= 12341 * 100 < 2^31, so ONE reduction per row is exact:
+// uint8 x uint8 products are summed four at a time with DP4A into a 32-bit accumulator.
+//
+// Mapping (v1).  Persistent CTAs pull surfaces from a global queue (early exit makes the work per
+// surface vary from 1 to bound-1 passes over M).  The vector lives in shared memory (ping-pong);
+// each warp owns UNROLL rows at a time, lanes stream 16-byte pieces of those rows from HBM with
+// non-allocating loads, and a warp-shuffle tree finishes each dot product.
+#pragma once
+#include "qfs_shape.cuh"
+
+template <int P>
+struct ChainCfg {
+    using S = Shape<P>;
+    static constexpr int NT = 512;
+    static constexpr int UNROLL = 4;
+    static constexpr int SMEM = 2 * S::pitch;
+};
+
+__device__ __forceinline__ uint4 ld_stream16(const uint4* p)
+{
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+template <int P>
+__global__ void __launch_bounds__(ChainCfg<P>::NT)
+k_chain(const uint8_t* __restrict__ M_all, const uint8_t* __restrict__ v0_all, const uint32_t* __restrict__ list,
+        int count, int max_steps, uint8_t* __restrict__ trace, int8_t* __restrict__ heights,
+        int8_t* __restrict__ iters, int* __restrict__ queue)
+{
+    using S = Shape<P>;
+    using C = ChainCfg<P>;
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ int s_slot;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = C::NT / 32;
+    constexpr int NCH = S::pitch / 16;
+
+    while (true) {
+        if (tid == 0) s_slot = atomicAdd(queue, 1);
+        __syncthreads();
+        const int slot = s_slot;
+        if (slot >= count) break;
+        const uint8_t* M = M_all + (size_t)slot * ((size_t)S::N * S::pitch);
+        uint8_t* va = smem;
+        uint8_t* vb = smem + S::pitch;
+        {
+            const uint4* src = reinterpret_cast<const uint4*>(v0_all + (size_t)slot * S::pitch);
+            for (int i = tid; i < NCH; i += C::NT) {
+                reinterpret_cast<uint4*>(va)[i] = src[i];
+                reinterpret_cast<uint4*>(vb)[i] = make_uint4(0, 0, 0, 0);
+            }
+        }
+        __syncthreads();
+        int height = 0, it = 0;
+        for (int step = 1; step <= max_steps; ++step) {
+            for (int row = warp * C::UNROLL; row < S::N; row += NW * C::UNROLL) {
+                uint32_t acc[C::UNROLL];
+#pragma unroll
+                for (int u = 0; u < C::UNROLL; ++u) acc[u] = 0;
+                for (int ch = lane; ch < NCH; ch += 32) {
+                    const uint4 v = reinterpret_cast<const uint4*>(va)[ch];
+                    uint4 m[C::UNROLL];
+#pragma unroll
+                    for (int u = 0; u < C::UNROLL; ++u) {
+                        const int rr = (row + u < S::N) ? row + u : S::N - 1;
+                        m[u] = ld_stream16(reinterpret_cast<const uint4*>(M + (size_t)rr * S::pitch) + ch);
+                    }
+#pragma unroll
+                    for (int u = 0; u < C::UNROLL; ++u) {
+                        acc[u] = __dp4a(m[u].x, v.x, acc[u]);
+                        acc[u] = __dp4a(m[u].y, v.y, acc[u]);
+                        acc[u] = __dp4a(m[u].z, v.z, acc[u]);
+                        acc[u] = __dp4a(m[u].w, v.w, acc[u]);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < C::UNROLL; ++u) {
+#pragma unroll
+                    for (int o = 16; o; o >>= 1) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], o);
+                }
+                if (lane == 0) {
+#pragma unroll
+                    for (int u = 0; u < C::UNROLL; ++u)
+                        if (row + u < S::N) vb[row + u] = (uint8_t)(acc[u] % (uint32_t)P);
+                }
+            }
+            __syncthreads();
+            ++it;
+            if (trace) {
+                uint8_t* tr = trace + ((size_t)slot * max_steps + (step - 1)) * S::N;
+                for (int i = tid; i < S::N; i += C::NT) tr[i] = vb[i];
+            }
+            { uint8_t* t = va; va = vb; vb = t; }
+            const bool hit = va[S::cap] != 0;
+            __syncthreads();
+            if (hit) { height = step + 1; break; }
+        }
+        if (tid == 0) {
+            const uint32_t sid = list ? list[slot] : (uint32_t)slot;
+            heights[sid] = (int8_t)height;
+            iters[sid] = (int8_t)it;
+        }
+    }
+}

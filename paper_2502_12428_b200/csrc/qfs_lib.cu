@@ -1,0 +1,669 @@
+// qfs_lib.cu -- host side of libqfs.so: context, workspaces, the chunked pipeline and the C ABI
+// declared in include/qfs.h.  One context drives one GPU; surfaces are independent, so multi-GPU
+// runs are N contexts over disjoint blocks of the batch with no collective.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/qfs.h"
+#include "qfs_chain.cuh"
+#include "qfs_delta.cuh"
+#include "qfs_matrix.cuh"
+#include "qfs_power.cuh"
+#include "qfs_shape.cuh"
+
+namespace {
+
+std::string g_create_error;
+
+struct DevBuf {
+    void* ptr = nullptr;
+    size_t cap = 0;
+    cudaError_t reserve(size_t bytes)
+    {
+        if (bytes <= cap) return cudaSuccess;
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        cap = 0;
+        cudaError_t e = cudaMalloc(&ptr, bytes);
+        if (e == cudaSuccess) cap = bytes;
+        return e;
+    }
+    void release()
+    {
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        cap = 0;
+    }
+    template <class T> T* as() const { return static_cast<T*>(ptr); }
+};
+
+enum { EV_COUNT = 8 };
+
+}  // namespace
+
+struct qfs_ctx {
+    int p = 0;
+    int device = 0;
+    int sm_count = 148;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev[EV_COUNT] = {};
+    cudaEvent_t ev_total[2] = {};
+    size_t workspace_limit = 0;
+    size_t chunk_override = 0;
+    std::string error;
+    qfs_stats stats = {};
+    // device state
+    DevBuf flags;                                   // int err, int queue, int count (+ pad)
+    DevBuf colinfo, groups;                         // per-p index tables for the matrix builder
+    DevBuf coeffs, heights, iters, list;            // batch-sized
+    DevBuf g, h, A, E, delta, M;                    // chunk-sized
+    DevBuf tapA, tapB;                              // staging for the stage taps
+    int* h_flags = nullptr;                         // pinned mirror of flags
+};
+
+namespace {
+
+int fail(qfs_ctx* ctx, int code, const char* fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (ctx) ctx->error = buf; else g_create_error = buf;
+    return code;
+}
+
+#define CU(call)                                                                                   \
+    do {                                                                                           \
+        cudaError_t e_ = (call);                                                                   \
+        if (e_ != cudaSuccess)                                                                     \
+            return fail(ctx, e_ == cudaErrorMemoryAllocation ? QFS_ENOMEM : QFS_ECUDA, "%s: %s",  \
+                        #call, cudaGetErrorString(e_));                                            \
+    } while (0)
+
+bool is_device_ptr(const void* p)
+{
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// single-block ordered stream compaction of {i : heights[i] < 0}
+__global__ void __launch_bounds__(1024) k_compact(const int8_t* __restrict__ heights, int B, uint32_t* __restrict__ list,
+                                                  int* __restrict__ count)
+{
+    __shared__ int s_warp[32];
+    __shared__ int s_base;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_base = 0;
+    __syncthreads();
+    for (int start = 0; start < B; start += 1024) {
+        const int i = start + tid;
+        const bool f = (i < B) && heights[i] < 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, f);
+        const int pre = __popc(bal & ((1u << lane) - 1));
+        if (lane == 0) s_warp[warp] = __popc(bal);
+        __syncthreads();
+        if (warp == 0) {
+            int v = s_warp[lane];
+            for (int o = 1; o < 32; o <<= 1) {
+                int t = __shfl_up_sync(0xffffffffu, v, o);
+                if (lane >= o) v += t;
+            }
+            s_warp[lane] = v;  // inclusive
+        }
+        __syncthreads();
+        const int wbase = warp ? s_warp[warp - 1] : 0;
+        if (f) list[s_base + wbase + pre] = (uint32_t)i;
+        __syncthreads();
+        if (tid == 0) s_base += s_warp[31];
+        __syncthreads();
+    }
+    if (tid == 0) *count = s_base;
+}
+
+// heights[i] == -1 (pending) -> 0 (infinity); used when bound < 2 (height.py:126-127)
+__global__ void k_pending_to_inf(int8_t* heights, int B)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < B && heights[i] < 0) heights[i] = 0;
+}
+
+template <int P>
+int build_tables(qfs_ctx* ctx)
+{
+    using S = Shape<P>;
+    std::vector<uint32_t> col(S::pitch, 0xFFFFFFFFu);
+    std::vector<uint16_t> grp(S::ngroups);
+    int c = 0, gidx = 0;
+    for (int c1 = 0; c1 <= S::d; ++c1)
+        for (int c2 = 0; c1 + c2 <= S::d; ++c2) {
+            grp[gidx++] = (uint16_t)(c1 | (c2 << 8));
+            for (int c3 = 0; c1 + c2 + c3 <= S::d; ++c3) col[c++] = (uint32_t)(c1 * (S::d + 1) + c2) | ((uint32_t)c3 << 16);
+        }
+    if (c != S::N || gidx != S::ngroups) return fail(ctx, QFS_EINVAL, "internal: basis enumeration mismatch");
+    CU(ctx->colinfo.reserve(col.size() * 4));
+    CU(ctx->groups.reserve(grp.size() * 2));
+    CU(cudaMemcpy(ctx->colinfo.ptr, col.data(), col.size() * 4, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(ctx->groups.ptr, grp.data(), grp.size() * 2, cudaMemcpyHostToDevice));
+    CU(cudaFuncSetAttribute(k_power<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, PowerCfg<P>::SMEM));
+    CU(cudaFuncSetAttribute(k_power<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, PowerCfg<P>::SMEM));
+    CU(cudaFuncSetAttribute(k_delta<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, DeltaCfg<P>::SMEM));
+    CU(cudaFuncSetAttribute(k_chain<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, ChainCfg<P>::SMEM));
+    return QFS_OK;
+}
+
+template <int P>
+size_t per_surface_bytes()
+{
+    using S = Shape<P>;
+    return (size_t)S::N * S::pitch + S::L_pad + 2 * (size_t)S::pitch + S::Nh_pad + S::NE_pad;
+}
+
+template <int P>
+int reserve_chunk(qfs_ctx* ctx, size_t cap)
+{
+    using S = Shape<P>;
+    CU(ctx->g.reserve(cap * S::pitch));
+    CU(ctx->A.reserve(cap * S::pitch));
+    CU(ctx->h.reserve(cap * S::Nh_pad));
+    CU(ctx->E.reserve(cap * S::NE_pad));
+    CU(ctx->delta.reserve(cap * S::L_pad));
+    CU(ctx->M.reserve(cap * (size_t)S::N * S::pitch));
+    return QFS_OK;
+}
+
+// ---- stage launchers (all on ctx->stream) ---------------------------------------------------
+template <int P>
+int launch_power_full(qfs_ctx* ctx, const uint8_t* d_coeffs, const uint32_t* d_list, int count, uint8_t* fedder)
+{
+    int* d_err = ctx->flags.as<int>();
+    k_power<P, true><<<count, PowerCfg<P>::NT, PowerCfg<P>::SMEM, ctx->stream>>>(
+        d_coeffs, d_list, count, nullptr, fedder, ctx->g.as<uint8_t>(), ctx->h.as<uint8_t>(), ctx->A.as<uint8_t>(),
+        ctx->E.as<uint8_t>(), d_err);
+    ctx->stats.kernel_launches++;
+    CU(cudaGetLastError());
+    return QFS_OK;
+}
+
+template <int P>
+int launch_delta(qfs_ctx* ctx, int count)
+{
+    k_delta<P><<<count, DeltaCfg<P>::NT, DeltaCfg<P>::SMEM, ctx->stream>>>(ctx->h.as<uint8_t>(), ctx->A.as<uint8_t>(),
+                                                                          ctx->E.as<uint8_t>(), ctx->delta.as<uint8_t>(), count);
+    ctx->stats.kernel_launches++;
+    CU(cudaGetLastError());
+    return QFS_OK;
+}
+
+template <int P>
+int launch_matrix(qfs_ctx* ctx, int count)
+{
+    using S = Shape<P>;
+    const unsigned grid = (unsigned)S::ngroups * (unsigned)count;
+    k_matrix<P><<<grid, MatrixCfg<P>::NT, 0, ctx->stream>>>(ctx->delta.as<uint8_t>(), ctx->colinfo.as<uint32_t>(),
+                                                          ctx->groups.as<uint16_t>(), ctx->M.as<uint8_t>(), count);
+    ctx->stats.kernel_launches++;
+    CU(cudaGetLastError());
+    return QFS_OK;
+}
+
+template <int P>
+int launch_chain(qfs_ctx* ctx, const uint8_t* v0, const uint32_t* d_list, int count, int max_steps, uint8_t* trace,
+                 int8_t* heights, int8_t* iters)
+{
+    int* d_queue = ctx->flags.as<int>() + 1;
+    CU(cudaMemsetAsync(d_queue, 0, sizeof(int), ctx->stream));
+    const int grid = std::min(count, ctx->sm_count * 2);
+    k_chain<P><<<grid, ChainCfg<P>::NT, ChainCfg<P>::SMEM, ctx->stream>>>(ctx->M.as<uint8_t>(), v0, d_list, count, max_steps,
+                                                                        trace, heights, iters, d_queue);
+    ctx->stats.kernel_launches++;
+    CU(cudaGetLastError());
+    return QFS_OK;
+}
+
+int check_device_flags(qfs_ctx* ctx)
+{
+    CU(cudaMemcpyAsync(ctx->h_flags, ctx->flags.ptr, 4 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    if (ctx->h_flags[0] & QFS_ERRBIT_INPUT)
+        return fail(ctx, QFS_EINVAL, "input violates a precondition: a coefficient >= p or the zero form");
+    if (ctx->h_flags[0] & QFS_ERRBIT_INVARIANT)
+        return fail(ctx, QFS_EINVARIANT, "Witt-carry numerator not divisible by p");
+    return QFS_OK;
+}
+
+float elapsed(cudaEvent_t a, cudaEvent_t b)
+{
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    return ms;
+}
+
+// ---- the pipeline ----------------------------------------------------------------------------
+template <int P>
+int run_heights(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, int bound, int8_t* heights, int8_t* iters, void* user_stream)
+{
+    using S = Shape<P>;
+    ctx->stats = qfs_stats{};
+    ctx->stats.surfaces = (int64_t)B;
+    if (B == 0) return QFS_OK;
+    if (B > 0x7fffffffULL) return fail(ctx, QFS_EINVAL, "batch too large");
+    CU(cudaSetDevice(ctx->device));
+    if (user_stream) {
+        CU(cudaEventRecord(ctx->ev[0], (cudaStream_t)user_stream));
+        CU(cudaStreamWaitEvent(ctx->stream, ctx->ev[0], 0));
+    }
+    const bool in_dev = is_device_ptr(coeffs), hout_dev = is_device_ptr(heights), iout_dev = is_device_ptr(iters);
+    const uint8_t* d_coeffs = coeffs;
+    if (!in_dev) {
+        CU(ctx->coeffs.reserve(B * 35));
+        CU(cudaMemcpyAsync(ctx->coeffs.ptr, coeffs, B * 35, cudaMemcpyHostToDevice, ctx->stream));
+        d_coeffs = ctx->coeffs.as<uint8_t>();
+    }
+    int8_t* d_heights = heights;
+    int8_t* d_iters = iters;
+    if (!hout_dev) { CU(ctx->heights.reserve(B)); d_heights = ctx->heights.as<int8_t>(); }
+    if (!iout_dev) { CU(ctx->iters.reserve(B)); d_iters = ctx->iters.as<int8_t>(); }
+    CU(ctx->list.reserve(B * sizeof(uint32_t)));
+    int* d_flags = ctx->flags.as<int>();
+    CU(cudaMemsetAsync(d_flags, 0, 4 * sizeof(int), ctx->stream));
+    CU(cudaMemsetAsync(d_iters, 0, B, ctx->stream));
+    CU(cudaEventRecord(ctx->ev_total[0], ctx->stream));
+
+    // pass 1: Fedder test for every surface (height 1 or pending)
+    CU(cudaEventRecord(ctx->ev[0], ctx->stream));
+    k_power<P, false><<<(unsigned)B, PowerCfg<P>::NT, PowerCfg<P>::SMEM, ctx->stream>>>(
+        d_coeffs, nullptr, (int)B, d_heights, nullptr, nullptr, nullptr, nullptr, nullptr, d_flags);
+    ctx->stats.kernel_launches++;
+    CU(cudaGetLastError());
+    CU(cudaEventRecord(ctx->ev[1], ctx->stream));
+    int hard = 0;
+    if (bound < 2) {
+        k_pending_to_inf<<<(unsigned)((B + 255) / 256), 256, 0, ctx->stream>>>(d_heights, (int)B);
+        ctx->stats.kernel_launches++;
+        int rc = check_device_flags(ctx);
+        if (rc) return rc;
+    } else {
+        k_compact<<<1, 1024, 0, ctx->stream>>>(d_heights, (int)B, ctx->list.as<uint32_t>(), d_flags + 2);
+        ctx->stats.kernel_launches++;
+        CU(cudaGetLastError());
+        int rc = check_device_flags(ctx);
+        if (rc) return rc;
+        hard = ctx->h_flags[2];
+    }
+    ctx->stats.ms_power += elapsed(ctx->ev[0], ctx->ev[1]);
+    ctx->stats.hard = hard;
+
+    if (hard > 0) {
+        // chunk capacity from the workspace budget
+        size_t limit = ctx->workspace_limit;
+        if (!limit) {
+            size_t fr = 0, tot = 0;
+            CU(cudaMemGetInfo(&fr, &tot));
+            size_t held = ctx->g.cap + ctx->A.cap + ctx->h.cap + ctx->E.cap + ctx->delta.cap + ctx->M.cap;
+            limit = (size_t)((double)(fr + held) * 0.4);
+        }
+        size_t cap = ctx->chunk_override ? ctx->chunk_override : std::max<size_t>(1, limit / per_surface_bytes<P>());
+        cap = std::min<size_t>(cap, (size_t)hard);
+        while (true) {
+            int rc = reserve_chunk<P>(ctx, cap);
+            if (rc == QFS_OK) break;
+            if (rc != QFS_ENOMEM || cap == 1) return rc;
+            cudaGetLastError();
+            cap = std::max<size_t>(1, cap / 2);
+        }
+        ctx->stats.chunk_capacity = (int64_t)cap;
+        const uint32_t* d_list = ctx->list.as<uint32_t>();
+        for (size_t done = 0; done < (size_t)hard; done += cap) {
+            const int cnt = (int)std::min<size_t>(cap, (size_t)hard - done);
+            int rc;
+            CU(cudaEventRecord(ctx->ev[0], ctx->stream));
+            if ((rc = launch_power_full<P>(ctx, d_coeffs, d_list + done, cnt, nullptr))) return rc;
+            CU(cudaEventRecord(ctx->ev[1], ctx->stream));
+            if ((rc = launch_delta<P>(ctx, cnt))) return rc;
+            CU(cudaEventRecord(ctx->ev[2], ctx->stream));
+            if ((rc = launch_matrix<P>(ctx, cnt))) return rc;
+            CU(cudaEventRecord(ctx->ev[3], ctx->stream));
+            if ((rc = launch_chain<P>(ctx, ctx->g.as<uint8_t>(), d_list + done, cnt, bound - 1, nullptr, d_heights, d_iters))) return rc;
+            CU(cudaEventRecord(ctx->ev[4], ctx->stream));
+            CU(cudaEventSynchronize(ctx->ev[4]));
+            ctx->stats.ms_power += elapsed(ctx->ev[0], ctx->ev[1]);
+            ctx->stats.ms_delta += elapsed(ctx->ev[1], ctx->ev[2]);
+            ctx->stats.ms_matrix += elapsed(ctx->ev[2], ctx->ev[3]);
+            ctx->stats.ms_matvec += elapsed(ctx->ev[3], ctx->ev[4]);
+            ctx->stats.chunks++;
+        }
+        int rc = check_device_flags(ctx);
+        if (rc) return rc;
+    }
+    CU(cudaEventRecord(ctx->ev_total[1], ctx->stream));
+    if (!hout_dev) CU(cudaMemcpyAsync(heights, d_heights, B, cudaMemcpyDeviceToHost, ctx->stream));
+    if (!iout_dev) CU(cudaMemcpyAsync(iters, d_iters, B, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    ctx->stats.ms_total = elapsed(ctx->ev_total[0], ctx->ev_total[1]);
+    if (hard > 0) {
+        // matvec steps: sum of iterations over hard surfaces (host outputs only; cheap)
+        if (!iout_dev) {
+            int64_t s = 0;
+            for (size_t i = 0; i < B; ++i) s += iters[i];
+            ctx->stats.matvec_steps = s;
+        }
+    }
+    return QFS_OK;
+}
+
+// copy a [B][n] dense host/device array into a padded device workspace and back
+int to_padded(qfs_ctx* ctx, DevBuf& buf, const uint8_t* src, size_t rows, size_t n, size_t pitch)
+{
+    CU(buf.reserve(rows * pitch));
+    CU(cudaMemsetAsync(buf.ptr, 0, rows * pitch, ctx->stream));
+    CU(cudaMemcpy2DAsync(buf.ptr, pitch, src, n, n, rows, cudaMemcpyDefault, ctx->stream));
+    return QFS_OK;
+}
+int from_padded(qfs_ctx* ctx, uint8_t* dst, const void* src, size_t rows, size_t n, size_t pitch)
+{
+    CU(cudaMemcpy2DAsync(dst, n, src, pitch, n, rows, cudaMemcpyDefault, ctx->stream));
+    return QFS_OK;
+}
+
+// Taps process the batch in slices small enough for the workspaces.
+template <int P>
+size_t tap_slice(qfs_ctx* ctx, size_t B, size_t bytes_per_row)
+{
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    size_t lim = ctx->workspace_limit ? ctx->workspace_limit : (size_t)(fr * 0.3);
+    return std::max<size_t>(1, std::min<size_t>(std::min<size_t>(B, 32768), lim / std::max<size_t>(1, bytes_per_row)));
+}
+
+template <int P>
+int run_stage_power(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, uint8_t* g, uint8_t* fedder)
+{
+    using S = Shape<P>;
+    CU(cudaSetDevice(ctx->device));
+    CU(cudaMemsetAsync(ctx->flags.ptr, 0, 4 * sizeof(int), ctx->stream));
+    const size_t slice = tap_slice<P>(ctx, B, per_surface_bytes<P>() - (size_t)S::N * S::pitch - S::L_pad + 64);
+    CU(ctx->tapA.reserve(slice * 35));
+    CU(ctx->tapB.reserve(slice));
+    for (size_t done = 0; done < B; done += slice) {
+        const int cnt = (int)std::min(slice, B - done);
+        CU(ctx->g.reserve((size_t)cnt * S::pitch));
+        CU(ctx->A.reserve((size_t)cnt * S::pitch));
+        CU(ctx->h.reserve((size_t)cnt * S::Nh_pad));
+        CU(ctx->E.reserve((size_t)cnt * S::NE_pad));
+        CU(cudaMemcpyAsync(ctx->tapA.ptr, coeffs + done * 35, (size_t)cnt * 35, cudaMemcpyDefault, ctx->stream));
+        int rc = launch_power_full<P>(ctx, ctx->tapA.as<uint8_t>(), nullptr, cnt, ctx->tapB.as<uint8_t>());
+        if (rc) return rc;
+        if (g && (rc = from_padded(ctx, g + done * S::N, ctx->g.ptr, cnt, S::N, S::pitch))) return rc;
+        if (fedder) CU(cudaMemcpyAsync(fedder + done, ctx->tapB.ptr, cnt, cudaMemcpyDefault, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+    }
+    return check_device_flags(ctx);
+}
+
+template <int P>
+int run_stage_delta(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, uint8_t* delta)
+{
+    using S = Shape<P>;
+    CU(cudaSetDevice(ctx->device));
+    CU(cudaMemsetAsync(ctx->flags.ptr, 0, 4 * sizeof(int), ctx->stream));
+    const size_t slice = tap_slice<P>(ctx, B, per_surface_bytes<P>() - (size_t)S::N * S::pitch + S::L_pad);
+    CU(ctx->tapA.reserve(slice * 35));
+    for (size_t done = 0; done < B; done += slice) {
+        const int cnt = (int)std::min(slice, B - done);
+        CU(ctx->g.reserve((size_t)cnt * S::pitch));
+        CU(ctx->A.reserve((size_t)cnt * S::pitch));
+        CU(ctx->h.reserve((size_t)cnt * S::Nh_pad));
+        CU(ctx->E.reserve((size_t)cnt * S::NE_pad));
+        CU(ctx->delta.reserve((size_t)cnt * S::L_pad));
+        CU(ctx->tapB.reserve((size_t)cnt * S::L_pad));
+        CU(cudaMemcpyAsync(ctx->tapA.ptr, coeffs + done * 35, (size_t)cnt * 35, cudaMemcpyDefault, ctx->stream));
+        int rc = launch_power_full<P>(ctx, ctx->tapA.as<uint8_t>(), nullptr, cnt, nullptr);
+        if (rc) return rc;
+        if ((rc = launch_delta<P>(ctx, cnt))) return rc;
+        dim3 grid(S::D + 1, cnt);
+        k_delta_flip<P><<<grid, 256, 0, ctx->stream>>>(ctx->delta.as<uint8_t>(), S::L_pad, ctx->tapB.as<uint8_t>(), S::L_pad);
+        CU(cudaGetLastError());
+        if ((rc = from_padded(ctx, delta + done * (size_t)S::L, ctx->tapB.ptr, cnt, S::L, S::L_pad))) return rc;
+        CU(cudaStreamSynchronize(ctx->stream));
+    }
+    return check_device_flags(ctx);
+}
+
+template <int P>
+int run_stage_matrix(qfs_ctx* ctx, const uint8_t* delta, size_t B, uint8_t* M)
+{
+    using S = Shape<P>;
+    CU(cudaSetDevice(ctx->device));
+    const size_t slice = tap_slice<P>(ctx, B, (size_t)S::N * S::pitch + 2 * (size_t)S::L_pad);
+    for (size_t done = 0; done < B; done += slice) {
+        const int cnt = (int)std::min(slice, B - done);
+        int rc = to_padded(ctx, ctx->tapB, delta + done * (size_t)S::L, cnt, S::L, S::L_pad);
+        if (rc) return rc;
+        CU(ctx->delta.reserve((size_t)cnt * S::L_pad));
+        CU(ctx->M.reserve((size_t)cnt * S::N * S::pitch));
+        dim3 grid(S::D + 1, cnt);
+        k_delta_flip<P><<<grid, 256, 0, ctx->stream>>>(ctx->tapB.as<uint8_t>(), S::L_pad, ctx->delta.as<uint8_t>(), S::L_pad);
+        CU(cudaGetLastError());
+        if ((rc = launch_matrix<P>(ctx, cnt))) return rc;
+        if ((rc = from_padded(ctx, M + done * (size_t)S::N * S::N, ctx->M.ptr, (size_t)cnt * S::N, S::N, S::pitch))) return rc;
+        CU(cudaStreamSynchronize(ctx->stream));
+    }
+    return QFS_OK;
+}
+
+template <int P>
+int run_stage_chain(qfs_ctx* ctx, const uint8_t* M, const uint8_t* v0, size_t B, int max_steps, uint8_t* trace,
+                    int8_t* heights, int8_t* iters)
+{
+    using S = Shape<P>;
+    CU(cudaSetDevice(ctx->device));
+    if (max_steps < 0) return fail(ctx, QFS_EINVAL, "max_steps must be >= 0");
+    const size_t slice = tap_slice<P>(ctx, B, (size_t)S::N * S::pitch + (size_t)(max_steps + 2) * S::pitch);
+    CU(ctx->heights.reserve(B));
+    CU(ctx->iters.reserve(B));
+    CU(cudaMemsetAsync(ctx->heights.ptr, 0, B, ctx->stream));
+    CU(cudaMemsetAsync(ctx->iters.ptr, 0, B, ctx->stream));
+    for (size_t done = 0; done < B; done += slice) {
+        const int cnt = (int)std::min(slice, B - done);
+        int rc = to_padded(ctx, ctx->M, M + done * (size_t)S::N * S::N, (size_t)cnt * S::N, S::N, S::pitch);
+        if (rc) return rc;
+        if ((rc = to_padded(ctx, ctx->g, v0 + done * S::N, cnt, S::N, S::pitch))) return rc;
+        uint8_t* d_trace = nullptr;
+        if (trace && max_steps > 0) {
+            CU(ctx->tapB.reserve((size_t)cnt * max_steps * S::N));
+            CU(cudaMemsetAsync(ctx->tapB.ptr, 0, (size_t)cnt * max_steps * S::N, ctx->stream));
+            d_trace = ctx->tapB.as<uint8_t>();
+        }
+        if ((rc = launch_chain<P>(ctx, ctx->g.as<uint8_t>(), nullptr, cnt, max_steps, d_trace,
+                                  ctx->heights.as<int8_t>() + done, ctx->iters.as<int8_t>() + done)))
+            return rc;
+        if (d_trace)
+            CU(cudaMemcpyAsync(trace + done * (size_t)max_steps * S::N, d_trace, (size_t)cnt * max_steps * S::N,
+                               cudaMemcpyDefault, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+    }
+    CU(cudaMemcpyAsync(heights, ctx->heights.ptr, B, cudaMemcpyDefault, ctx->stream));
+    CU(cudaMemcpyAsync(iters, ctx->iters.ptr, B, cudaMemcpyDefault, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return QFS_OK;
+}
+
+template <int P>
+void fill_shape(qfs_shape* s)
+{
+    using S = Shape<P>;
+    s->p = P; s->d = S::d; s->D = S::D; s->N = S::N; s->pitch = S::pitch; s->cap = S::cap; s->L = S::L;
+}
+
+#define QFS_DISPATCH(p, expr3, expr5, expr7, expr11, bad) \
+    switch (p) {                                          \
+        case 3: return expr3;                             \
+        case 5: return expr5;                             \
+        case 7: return expr7;                             \
+        case 11: return expr11;                           \
+        default: return bad;                              \
+    }
+
+}  // namespace
+
+extern "C" {
+
+int qfs_version(void) { return QFS_ABI_VERSION; }
+
+int qfs_get_shape(int p, qfs_shape* out)
+{
+    qfs_shape tmp;
+    qfs_shape* s = out ? out : &tmp;
+    switch (p) {
+        case 3: fill_shape<3>(s); return QFS_OK;
+        case 5: fill_shape<5>(s); return QFS_OK;
+        case 7: fill_shape<7>(s); return QFS_OK;
+        case 11: fill_shape<11>(s); return QFS_OK;
+        default: return QFS_EINVAL;
+    }
+}
+
+const char* qfs_last_error(const qfs_ctx* ctx) { return ctx ? ctx->error.c_str() : g_create_error.c_str(); }
+
+void qfs_destroy(qfs_ctx* ctx)
+{
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    DevBuf* bufs[] = {&ctx->flags, &ctx->colinfo, &ctx->groups, &ctx->coeffs, &ctx->heights, &ctx->iters, &ctx->list,
+                      &ctx->g, &ctx->h, &ctx->A, &ctx->E, &ctx->delta, &ctx->M, &ctx->tapA, &ctx->tapB};
+    for (DevBuf* b : bufs) b->release();
+    for (auto& e : ctx->ev) if (e) cudaEventDestroy(e);
+    for (auto& e : ctx->ev_total) if (e) cudaEventDestroy(e);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    if (ctx->h_flags) cudaFreeHost(ctx->h_flags);
+    delete ctx;
+}
+
+int qfs_create(int p, int device, size_t max_batch, qfs_ctx** out)
+{
+    (void)max_batch;
+    if (!out) return fail(nullptr, QFS_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (qfs_get_shape(p, nullptr) != QFS_OK)
+        return fail(nullptr, QFS_EINVAL, "p=%d is not supported by this build (supported: 3, 5, 7, 11)", p);
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0)
+        return fail(nullptr, QFS_ECUDA, "no CUDA device available: %s", cudaGetErrorString(e));
+    if (device < 0 || device >= ndev) return fail(nullptr, QFS_EINVAL, "device %d out of range (0..%d)", device, ndev - 1);
+    qfs_ctx* ctx = new qfs_ctx;
+    ctx->p = p;
+    ctx->device = device;
+    auto bail = [&](int rc) { g_create_error = ctx->error; qfs_destroy(ctx); return rc; };
+#define CUC(call)                                                                                          \
+    do {                                                                                                   \
+        cudaError_t e_ = (call);                                                                           \
+        if (e_ != cudaSuccess) { fail(ctx, QFS_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); return bail(QFS_ECUDA); } \
+    } while (0)
+    CUC(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CUC(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10) {
+        fail(ctx, QFS_ECUDA, "device %d is sm_%d%d; this library is built for sm_100a (B200) only", device, prop.major, prop.minor);
+        return bail(QFS_ECUDA);
+    }
+    ctx->sm_count = prop.multiProcessorCount;
+    CUC(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    for (auto& ev : ctx->ev) CUC(cudaEventCreate(&ev));
+    for (auto& ev : ctx->ev_total) CUC(cudaEventCreate(&ev));
+    CUC(cudaMallocHost(&ctx->h_flags, 4 * sizeof(int)));
+    CUC(ctx->flags.reserve(4 * sizeof(int)));
+    CUC(cudaMemset(ctx->flags.ptr, 0, 4 * sizeof(int)));
+#undef CUC
+    int rc;
+    switch (p) {
+        case 3: rc = build_tables<3>(ctx); break;
+        case 5: rc = build_tables<5>(ctx); break;
+        case 7: rc = build_tables<7>(ctx); break;
+        default: rc = build_tables<11>(ctx); break;
+    }
+    if (rc) return bail(rc);
+    *out = ctx;
+    return QFS_OK;
+}
+
+int qfs_set_workspace_limit(qfs_ctx* ctx, size_t bytes)
+{
+    if (!ctx) return QFS_EINVAL;
+    ctx->workspace_limit = bytes;
+    return QFS_OK;
+}
+
+int qfs_set_chunk(qfs_ctx* ctx, size_t n)
+{
+    if (!ctx) return QFS_EINVAL;
+    ctx->chunk_override = n;
+    return QFS_OK;
+}
+
+int qfs_get_stats(const qfs_ctx* ctx, qfs_stats* out)
+{
+    if (!ctx || !out) return QFS_EINVAL;
+    *out = ctx->stats;
+    return QFS_OK;
+}
+
+int qfs_heights(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, int bound, int8_t* heights, int8_t* iters, void* stream)
+{
+    if (!ctx) return QFS_EINVAL;
+    if (B && (!coeffs || !heights || !iters)) return fail(ctx, QFS_EINVAL, "NULL buffer");
+    if (bound < 1 || bound > 127) return fail(ctx, QFS_EINVAL, "bound must be in 1..127, got %d", bound);
+    QFS_DISPATCH(ctx->p, run_heights<3>(ctx, coeffs, B, bound, heights, iters, stream),
+                 run_heights<5>(ctx, coeffs, B, bound, heights, iters, stream),
+                 run_heights<7>(ctx, coeffs, B, bound, heights, iters, stream),
+                 run_heights<11>(ctx, coeffs, B, bound, heights, iters, stream), QFS_EINVAL)
+}
+
+int qfs_stage_power(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, uint8_t* g, uint8_t* fedder)
+{
+    if (!ctx) return QFS_EINVAL;
+    if (B && !coeffs) return fail(ctx, QFS_EINVAL, "NULL buffer");
+    QFS_DISPATCH(ctx->p, run_stage_power<3>(ctx, coeffs, B, g, fedder), run_stage_power<5>(ctx, coeffs, B, g, fedder),
+                 run_stage_power<7>(ctx, coeffs, B, g, fedder), run_stage_power<11>(ctx, coeffs, B, g, fedder), QFS_EINVAL)
+}
+
+int qfs_stage_delta(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, uint8_t* delta)
+{
+    if (!ctx) return QFS_EINVAL;
+    if (B && (!coeffs || !delta)) return fail(ctx, QFS_EINVAL, "NULL buffer");
+    QFS_DISPATCH(ctx->p, run_stage_delta<3>(ctx, coeffs, B, delta), run_stage_delta<5>(ctx, coeffs, B, delta),
+                 run_stage_delta<7>(ctx, coeffs, B, delta), run_stage_delta<11>(ctx, coeffs, B, delta), QFS_EINVAL)
+}
+
+int qfs_stage_matrix(qfs_ctx* ctx, const uint8_t* delta, size_t B, uint8_t* M)
+{
+    if (!ctx) return QFS_EINVAL;
+    if (B && (!delta || !M)) return fail(ctx, QFS_EINVAL, "NULL buffer");
+    QFS_DISPATCH(ctx->p, run_stage_matrix<3>(ctx, delta, B, M), run_stage_matrix<5>(ctx, delta, B, M),
+                 run_stage_matrix<7>(ctx, delta, B, M), run_stage_matrix<11>(ctx, delta, B, M), QFS_EINVAL)
+}
+
+int qfs_stage_matvec_chain(qfs_ctx* ctx, const uint8_t* M, const uint8_t* v0, size_t B, int max_steps, uint8_t* trace,
+                           int8_t* heights, int8_t* iters)
+{
+    if (!ctx) return QFS_EINVAL;
+    if (B && (!M || !v0 || !heights || !iters)) return fail(ctx, QFS_EINVAL, "NULL buffer");
+    QFS_DISPATCH(ctx->p, run_stage_chain<3>(ctx, M, v0, B, max_steps, trace, heights, iters),
+                 run_stage_chain<5>(ctx, M, v0, B, max_steps, trace, heights, iters),
+                 run_stage_chain<7>(ctx, M, v0, B, max_steps, trace, heights, iters),
+                 run_stage_chain<11>(ctx, M, v0, B, max_steps, trace, heights, iters), QFS_EINVAL)
+}
+
+}  // extern "C"

@@ -1,0 +1,52 @@
+// qfs_shape.cuh -- index conventions and per-prime shape constants shared by every kernel.
+//
+// Dense layout of a degree-`deg` form in x1..x4 ("lex"): monomials in lex-ascending order with
+// x1 most significant, index 0 = x4^deg (reference: monomials.py:182-196 `wics`, :208-276
+// `MonomialBasis`).  Closed form (verified against MonomialBasis):
+//   rank(a1,a2,a3,a4) = rowbase(deg,a1,a2) + a3,
+//   rowbase(deg,a1,a2) = C(deg+3,3)-C(deg-a1+3,3) + C(deg-a1+2,2)-C(deg-a1-a2+2,2).
+// A "run" is the set of monomials sharing (a1,a2): deg-a1-a2+1 consecutive entries.
+//
+// Internal layout of Delta ("lex43"): same run structure, but inside a run entries are ordered
+// by a4 instead of a3 (the run is stored reversed).  With it every run of an operator-matrix
+// row is a FORWARD contiguous copy of a piece of a Delta run (see qfs_matrix.cuh).
+#pragma once
+#include <stdint.h>
+
+#if defined(__CUDACC__)
+#define QFS_HD __host__ __device__ __forceinline__
+#else
+#define QFS_HD inline
+#endif
+
+QFS_HD constexpr int qc2(int n) { return n >= 2 ? n * (n - 1) / 2 : 0; }
+QFS_HD constexpr int qc3(int n) { return n >= 3 ? n * (n - 1) * (n - 2) / 6 : 0; }
+QFS_HD constexpr int qrowbase(int deg, int a1, int a2)
+{
+    return qc3(deg + 3) - qc3(deg - a1 + 3) + qc2(deg - a1 + 2) - qc2(deg - a1 - a2 + 2);
+}
+QFS_HD constexpr int qround16(int n) { return (n + 15) & ~15; }
+
+template <int P>
+struct Shape {
+    static constexpr int p = P;
+    static constexpr int psq = P * P;
+    static constexpr int d = 4 * (P - 1);                 // deg g = deg f^(p-1)
+    static constexpr int dh = (P > 2) ? 4 * (P - 2) : 0;  // deg h = deg f^(p-2)
+    static constexpr int dE = 4 * P;                      // deg E = deg Delta_1(f)
+    static constexpr int D = P * d;                       // deg Delta
+    static constexpr int N = qc3(d + 3);
+    static constexpr int Nh = qc3(dh + 3);
+    static constexpr int NE = qc3(dE + 3);
+    static constexpr int L = qc3(D + 3);
+    static constexpr int pitch = qround16(N);   // row pitch of M and stride of N-vectors
+    static constexpr int Nh_pad = qround16(Nh);
+    static constexpr int NE_pad = qround16(NE);
+    static constexpr int L_pad = qround16(L);
+    static constexpr int cap = qrowbase(d, P - 1, P - 1) + P - 1;
+    static constexpr int ngroups = (d + 1) * (d + 2) / 2;  // (r1,r2) row groups of M
+};
+
+// error bits raised by kernels into the context's device flag word
+#define QFS_ERRBIT_INPUT 1      // coefficient >= p, or the zero form
+#define QFS_ERRBIT_INVARIANT 2  // Witt-carry numerator not divisible by p
