@@ -1,0 +1,372 @@
+#!/usr/bin/env python3
+"""bench.py -- quartic-K3 quasi-F-split heights/sec on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--p 5] [--batch 100000] [--impl reference]
+
+A "step" is one pass of the hot path (qfs_heights: power chain -> Witt carry -> operator matrix ->
+matvec chain with early exit) over one batch of seeded synthetic quartics, generated with the
+reference's sampler recipe (numpy default_rng([seed, worker]), one integers(0,p,35) draw per
+surface, zero draws redrawn; search.py:92-98,103).  Default workload = BASELINE.json configs[1]:
+100k random quartics over F_5 on one B200; the F_7 100k batch (configs[2]) is measured in the same
+run and reported under "also".
+
+One JSON line on stdout (rank 0).  `value` = whole-job surfaces/s with inputs resident in HBM;
+`e2e` = the same through the public API with pinned HOST buffers (H2D/D2H inside the timed region);
+`roofline` = the dominant kernel against the measured HBM peak; `cpu_baseline` = the C oracle
+(oracle/, a port of the reference's CPU algorithm) on this box's host cores.
+`--impl reference` times that CPU port alone (the reference itself is pure Python under
+/root/reference and cannot travel to the GPU box).
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PAPER_RATE = {5: 1400.0, 7: 180.0}  # BASELINE.md section 1 (2080 Ti), surfaces that take the full operator path
+SHAPES = {3: (165, 2925), 5: (969, 91881), 7: (2925, 818805), 11: (12341, 14391741)}  # N, L
+
+
+def sample_block(p, count, seed, worker):
+    """`count` coefficient vectors exactly as search._worker_block draws them (search.py:103,92-98)."""
+    rng = np.random.default_rng([seed, worker])
+    out = np.empty((count, 35), dtype=np.uint8)
+    for i in range(count):
+        while True:
+            v = rng.integers(0, p, size=35)
+            if v.any():
+                break
+        out[i] = v
+    return out
+
+
+def cached_block(p, count, seed, worker):
+    d = os.path.join(ROOT, "bench_cache")
+    path = os.path.join(d, f"coeffs_p{p}_s{seed}_w{worker}_{count}.npy")
+    try:
+        if os.path.exists(path):
+            return np.load(path)
+    except Exception:
+        pass
+    c = sample_block(p, count, seed, worker)
+    try:
+        os.makedirs(d, exist_ok=True)
+        np.save(path, c)
+    except Exception:
+        pass
+    return c
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            j = json.load(fh)
+        return float(j["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy bandwidth)"
+    except Exception:
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms while the timed region runs."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.lines = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._pump, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _pump(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def algorithmic_bytes(p, iters_hard):
+    """Per-kernel algorithmic HBM bytes for a batch (uint8 entries)."""
+    N, L = SHAPES[p]
+    hard = int(iters_hard.size)
+    ksum = int(iters_hard.sum())
+    return {
+        "delta": hard * L,                          # Delta written once
+        "matrix": hard * (N * N + L),               # Delta gathered, M written once
+        "matvec": ksum * N * N + (ksum + hard) * N,  # M streamed once per operator application
+        "total": hard * (N * N + 2 * L) + ksum * N * N + (ksum + hard) * N,
+    }
+
+
+def cpu_baseline(p, coeffs, budget_s):
+    """C oracle (port of the reference CPU algorithm) on all host threads, on a bounded prefix."""
+    import oracle
+    threads = oracle.max_threads()
+    pilot = min(len(coeffs), 8 * threads)
+    t0 = time.perf_counter()
+    oracle.heights_batch(coeffs[:pilot], p, 10, threads)
+    dt = max(time.perf_counter() - t0, 1e-4)
+    n = int(min(len(coeffs), max(pilot, pilot * budget_s / dt)))
+    t0 = time.perf_counter()
+    hs, _ = oracle.heights_batch(coeffs[:n], p, 10, threads)
+    dt = time.perf_counter() - t0
+    hard = int((hs != 1).sum())
+    return {"value": n / dt, "unit": "surfaces/s", "cores": threads, "kind": "port",
+            "hard_per_s": hard / dt,
+            "sample": f"first {n} surfaces of the same seeded F_{p} batch ({hard} with height>=2), "
+                      f"oracle/qfs_oracle.c (C port of qfsplit height_matrix), OpenMP over surfaces, {dt:.1f} s"}, hs
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    p = args.p
+    coeffs = cached_block(p, min(args.batch, 20000), args.seed, 0)
+    import oracle
+    threads = oracle.max_threads()
+    # size one step to ~ (120 s / (steps+warmup)) of CPU work
+    pilot = 8 * threads
+    t0 = time.perf_counter()
+    oracle.heights_batch(coeffs[:pilot], p, 10, threads)
+    per = (time.perf_counter() - t0) / pilot
+    budget = 120.0 / max(1, args.steps + args.warmup)
+    n = int(max(pilot, min(len(coeffs), budget / per)))
+    for _ in range(args.warmup):
+        oracle.heights_batch(coeffs[:n], p, 10, threads)
+    t0 = time.perf_counter()
+    hard = 0
+    for _ in range(args.steps):
+        hs, _ = oracle.heights_batch(coeffs[:n], p, 10, threads)
+        hard = int((hs != 1).sum())
+    dt = time.perf_counter() - t0
+    val = n * args.steps / dt
+    sample = (f"each step = first {n} surfaces of the seeded F_{p} batch ({hard} with height>=2) through "
+              f"oracle/qfs_oracle.c (C port of the reference's qfsplit.height_matrix; the reference is pure "
+              f"Python and is absent on the GPU box) on {threads} host threads")
+    line = {
+        "impl": "reference", "metric": "quartic K3 heights/sec", "value": val, "unit": "surfaces/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": f"{args.batch} seeded random quartics over F_{p} (sampled: {n}/step)", "p": p, "bound": 10},
+        "cpu_baseline": {"value": val, "unit": "surfaces/s", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": val, "unit": "surfaces/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line))
+
+
+def measure_gpu(p, batch, steps, warmup, seed, rank, world, device, dist):
+    import torch
+    from paper_2502_12428_b200.engine import get_engine
+    eng = get_engine(p, device)
+    host = cached_block(p, batch, seed, rank)
+    pinned = torch.from_numpy(host).pin_memory()
+    dev = pinned.to(f"cuda:{device}", non_blocking=False)
+    hs = torch.empty(batch, dtype=torch.int8, device=dev.device)
+    its = torch.empty(batch, dtype=torch.int8, device=dev.device)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize(device)
+
+    for _ in range(warmup):
+        eng.heights(dev, 10, out=(hs, its))
+    stage = {"ms_power": 0.0, "ms_delta": 0.0, "ms_matrix": 0.0, "ms_matvec": 0.0, "ms_total": 0.0}
+    launches = 0
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(device)
+    sampler.start()
+    e0.record()
+    for _ in range(steps):
+        eng.heights(dev, 10, out=(hs, its))
+        st = eng.stats()
+        for k in stage:
+            stage[k] += st[k]
+        launches += st["kernel_launches"]
+    e1.record()
+    barrier()
+    clocks = sampler.stop()
+    ms = e0.elapsed_time(e1)
+    st = eng.stats()
+
+    # end to end through the public API with pinned host buffers
+    h_hs = torch.empty(batch, dtype=torch.int8).pin_memory().numpy()
+    h_its = torch.empty(batch, dtype=torch.int8).pin_memory().numpy()
+    h_in = pinned.numpy()
+    e2e_steps = max(1, min(steps, 10))
+    eng.heights(h_in, 10, out=(h_hs, h_its))
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        eng.heights(h_in, 10, out=(h_hs, h_its))
+    torch.cuda.synchronize(device)
+    e2e_s = time.perf_counter() - t0
+
+    heights = hs.cpu().numpy()
+    iters = its.cpu().numpy()
+    assert np.array_equal(heights, h_hs) and np.array_equal(iters, h_its)
+    if dist is not None:
+        t = torch.tensor([ms, e2e_s], dtype=torch.float64, device=dev.device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, e2e_s = float(t[0]), float(t[1])
+    return {"ms": ms, "e2e_s": e2e_s, "e2e_steps": e2e_steps, "stage": stage, "launches": launches, "stats": st,
+            "heights": heights, "iters": iters, "coeffs": host, "clocks": clocks}
+
+
+def gpu_line(args, p, res, world, with_cpu):
+    batch, steps = args.batch, res["steps"]
+    peak, peak_src = measured_peaks()
+    heights, iters = res["heights"], res["iters"]
+    hard_mask = heights != 1
+    hard = int(hard_mask.sum())
+    ab = algorithmic_bytes(p, iters[hard_mask].astype(np.int64))
+    ms_step = res["ms"] / steps
+    value = world * batch * steps / (res["ms"] * 1e-3)
+    stage = {k: v / steps for k, v in res["stage"].items()}
+    kernels = {"delta": ("k_delta", stage["ms_delta"], ab["delta"]),
+               "matrix": ("k_matrix", stage["ms_matrix"], ab["matrix"]),
+               "matvec": ("k_chain", stage["ms_matvec"], ab["matvec"])}
+    top = max(kernels, key=lambda k: kernels[k][1])
+    name, kms, kbytes = kernels[top]
+    ach = kbytes / (kms * 1e-3) / 1e9 if kms > 0 else 0.0
+    N, L = SHAPES[p]
+    line = {
+        "metric": "quartic K3 heights/sec", "value": value, "unit": "surfaces/s", "n_gpus": world,
+        "steps": steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": (value * hard / batch) / PAPER_RATE[p] if p in PAPER_RATE else None,
+        "dtype": "u8", "data": "synthetic",
+        "config": {
+            "workload": f"{batch} seeded random quartics over F_{p} per GPU ({N}x{N} operator), bound 10",
+            "p": p, "batch_per_gpu": batch, "seed": args.seed, "parallelism": f"{world} independent shards, no collective",
+            "l2": f"working set per step {ab['total'] / 1e9:.1f} GB >> 126 MB L2 (no flush needed)",
+            "vs_baseline_note": "hard (height>=2) surfaces/s over the paper's ~%d/s on a 2080 Ti (BASELINE.md s1)" % PAPER_RATE.get(p, 0),
+        },
+        "hard_fraction": hard / batch,
+        "hard_per_s": value * hard / batch,
+        "height_histogram": {str(k): int(v) for k, v in enumerate(np.bincount(heights.astype(np.int64), minlength=2)) if v},
+        "stage_ms_per_step": stage,
+        "roofline": {"bound": "hbm", "kernel": name, "achieved": ach, "peak": peak, "unit": "GB/s",
+                     "frac": ach / peak, "traffic": None, "algorithmic_bytes_per_launch": kbytes / max(1, res["stats"]["chunks"]),
+                     "launches_per_step": res["stats"]["chunks"], "ms_per_step": kms, "peak_source": peak_src,
+                     "all_kernels": {k: {"ms": v[1], "GBps": (v[2] / (v[1] * 1e-3) / 1e9 if v[1] > 0 else 0.0)} for k, v in kernels.items()}},
+        "roofline_pipeline": {"algorithmic_bytes_per_step": ab["total"], "achieved": ab["total"] / (ms_step * 1e-3) / 1e9,
+                              "peak": peak, "unit": "GB/s", "frac": ab["total"] / (ms_step * 1e-3) / 1e9 / peak},
+        "e2e": {"value": world * batch * res["e2e_steps"] / res["e2e_s"], "unit": "surfaces/s",
+                "h2d_bytes_per_step": batch * 35, "d2h_bytes_per_step": 2 * batch},
+        "gpu_launches": int(res["launches"]),
+        "clocks": res["clocks"],
+    }
+    if with_cpu:
+        cb, ohs = cpu_baseline(p, res["coeffs"], args.cpu_seconds)
+        n = len(ohs)
+        cb["parity_on_sample"] = bool(np.array_equal(ohs, heights[:n]))
+        line["cpu_baseline"] = cb
+    return line
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200")
+    ap.add_argument("--p", type=int, default=5)
+    ap.add_argument("--batch", type=int, default=100000)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-also", action="store_true", help="skip the secondary F_7 measurement")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 0)
+
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist_mod
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local)
+        dist_mod.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        dist = dist_mod
+    elif args.gpus > 1 and "RANK" not in os.environ:
+        # convenience: relaunch under torchrun
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", "29531"] + sys.argv
+        sys.exit(subprocess.call(cmd))
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (there is no CPU fallback); use --impl reference for the CPU arm")
+    torch.cuda.set_device(local)
+
+    res = measure_gpu(args.p, args.batch, args.steps, max(args.warmup, 3), args.seed, rank, world, local, dist)
+    res["steps"] = args.steps
+    line = None
+    if rank == 0:
+        line = gpu_line(args, args.p, res, world, with_cpu=True)
+    if not args.no_also and args.p == 5:
+        k7 = max(2, args.steps // 3)
+        res7 = measure_gpu(7, args.batch, k7, 3, args.seed, rank, world, local, dist)
+        res7["steps"] = k7
+        if rank == 0:
+            l7 = gpu_line(args, 7, res7, world, with_cpu=(world == 1))
+            keep = ("value", "unit", "ms_per_step", "steps", "hard_per_s", "vs_baseline", "stage_ms_per_step", "roofline",
+                    "roofline_pipeline", "e2e", "cpu_baseline", "height_histogram")
+            line["also"] = {"F_7": {k: l7[k] for k in keep if k in l7}}
+    if rank == 0:
+        print(json.dumps(line))
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -61,6 +61,7 @@ struct qfs_ctx {
     // device state
     DevBuf flags;                                   // int err, int queue, int count (+ pad)
     DevBuf colinfo, groups;                         // per-p index tables for the matrix builder
+    DevBuf unrank;                                  // per-p unrank tables for the power chain
     DevBuf coeffs, heights, iters, list;            // batch-sized
     DevBuf g, h, A, E, delta, M;                    // chunk-sized
     DevBuf tapA, tapB;                              // staging for the stage taps
@@ -156,8 +157,20 @@ int build_tables(qfs_ctx* ctx)
     CU(ctx->groups.reserve(grp.size() * 2));
     CU(cudaMemcpy(ctx->colinfo.ptr, col.data(), col.size() * 4, cudaMemcpyHostToDevice));
     CU(cudaMemcpy(ctx->groups.ptr, grp.data(), grp.size() * 2, cudaMemcpyHostToDevice));
-    CU(cudaFuncSetAttribute(k_power<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, PowerCfg<P>::SMEM));
-    CU(cudaFuncSetAttribute(k_power<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, PowerCfg<P>::SMEM));
+    {
+        std::vector<uint32_t> un;
+        for (int k = 1; k <= P; ++k) {
+            const int deg = 4 * k;
+            if ((int)un.size() != qunrank_offset(k)) return fail(ctx, QFS_EINVAL, "internal: unrank offset mismatch");
+            for (int a1 = 0; a1 <= deg; ++a1)
+                for (int a2 = 0; a1 + a2 <= deg; ++a2)
+                    for (int a3 = 0; a1 + a2 + a3 <= deg; ++a3) un.push_back((uint32_t)a1 | ((uint32_t)a2 << 8) | ((uint32_t)a3 << 16));
+        }
+        CU(ctx->unrank.reserve(un.size() * 4));
+        CU(cudaMemcpy(ctx->unrank.ptr, un.data(), un.size() * 4, cudaMemcpyHostToDevice));
+    }
+    CU(cudaFuncSetAttribute(k_fedder<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, PowerCfg<P>::FED_SMEM));
+    CU(cudaFuncSetAttribute(k_power_full<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, PowerCfg<P>::FULL_SMEM));
     CU(cudaFuncSetAttribute(k_delta<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, DeltaCfg<P>::SMEM));
     CU(cudaFuncSetAttribute(k_chain<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, ChainCfg<P>::SMEM));
     return QFS_OK;
@@ -188,9 +201,9 @@ template <int P>
 int launch_power_full(qfs_ctx* ctx, const uint8_t* d_coeffs, const uint32_t* d_list, int count, uint8_t* fedder)
 {
     int* d_err = ctx->flags.as<int>();
-    k_power<P, true><<<count, PowerCfg<P>::NT, PowerCfg<P>::SMEM, ctx->stream>>>(
-        d_coeffs, d_list, count, nullptr, fedder, ctx->g.as<uint8_t>(), ctx->h.as<uint8_t>(), ctx->A.as<uint8_t>(),
-        ctx->E.as<uint8_t>(), d_err);
+    k_power_full<P><<<count, PowerCfg<P>::FULL_NT, PowerCfg<P>::FULL_SMEM, ctx->stream>>>(
+        d_coeffs, d_list, count, ctx->unrank.as<uint32_t>(), fedder, ctx->g.as<uint8_t>(), ctx->h.as<uint8_t>(),
+        ctx->A.as<uint8_t>(), ctx->E.as<uint8_t>(), d_err);
     ctx->stats.kernel_launches++;
     CU(cudaGetLastError());
     return QFS_OK;
@@ -283,8 +296,8 @@ int run_heights(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, int bound, int8_t
 
     // pass 1: Fedder test for every surface (height 1 or pending)
     CU(cudaEventRecord(ctx->ev[0], ctx->stream));
-    k_power<P, false><<<(unsigned)B, PowerCfg<P>::NT, PowerCfg<P>::SMEM, ctx->stream>>>(
-        d_coeffs, nullptr, (int)B, d_heights, nullptr, nullptr, nullptr, nullptr, nullptr, d_flags);
+    k_fedder<P><<<(unsigned)((B + PowerCfg<P>::FED_WARPS - 1) / PowerCfg<P>::FED_WARPS), PowerCfg<P>::FED_WARPS * 32,
+                  PowerCfg<P>::FED_SMEM, ctx->stream>>>(d_coeffs, (int)B, ctx->unrank.as<uint32_t>(), d_heights, d_flags);
     ctx->stats.kernel_launches++;
     CU(cudaGetLastError());
     CU(cudaEventRecord(ctx->ev[1], ctx->stream));
@@ -541,7 +554,7 @@ void qfs_destroy(qfs_ctx* ctx)
 {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
-    DevBuf* bufs[] = {&ctx->flags, &ctx->colinfo, &ctx->groups, &ctx->coeffs, &ctx->heights, &ctx->iters, &ctx->list,
+    DevBuf* bufs[] = {&ctx->flags, &ctx->colinfo, &ctx->groups, &ctx->unrank, &ctx->coeffs, &ctx->heights, &ctx->iters, &ctx->list,
                       &ctx->g, &ctx->h, &ctx->A, &ctx->E, &ctx->delta, &ctx->M, &ctx->tapA, &ctx->tapB};
     for (DevBuf* b : bufs) b->release();
     for (auto& e : ctx->ev) if (e) cudaEventDestroy(e);

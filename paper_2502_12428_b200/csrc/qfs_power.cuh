@@ -1,173 +1,319 @@
-// qfs_power.cuh -- stage 1: the power chain mod p^2, one CTA per surface.
+// qfs_power.cuh -- stage 1: powers of the quartic.
 //
 // Replaces  power_mod_p(f, p-1)            polyring.py:253-272  (-> g, Fedder test polyring.py:316-332)
 // and feeds the factorised Witt carry that replaces delta1 / power_mod_small
 //                                           polyring.py:335-401, nttpower.py:447-507.
 //
-// With tau(a) = a^p mod p^2 (Teichmuller representative) and f_T = sum tau(a_J) x^J the chain
-//     f_T^2, f_T^3, ..., f_T^p   (each step: dense product with the <= 35-term f_T, mod p^2)
-// yields  H = f_T^(p-2), G = f_T^(p-1), Pw = f_T^p  and from them, exactly:
-//     h = H mod p = f^(p-2),   g = G mod p = f^(p-1),
-//     A[I] = ((G[I] - tau(g[I])) mod p^2)/p,     E[J] = ((Pw[J] - [p|J] tau(a_{J/p})) mod p^2)/p  (= Delta_1(f)).
-// The divisions are exact; a violation raises QFS_ERRBIT_INVARIANT (the reference's
-// InternalInvariantError, polyring.py:397-398).  All arithmetic is integer: residues < p^2 <= 121
-// in uint8, products accumulated in uint32 (35 * 120^2 < 2^32), one reduction per output.
+// Two kernels:
 //
-// FULL = false: chain only up to H, then the single coefficient G[cap] -> height 1 or "pending".
-// FULL = true : whole chain; writes g, h, A, E for the surface into the chunk workspaces.
+// k_fedder (every surface, one WARP per surface, arithmetic mod p).
+//   Height 1 <=> the coefficient of (x1x2x3x4)^(p-1) in f^(p-1) is nonzero.  Only that one
+//   coefficient is needed, so the chain f^2, f^3, ... is computed in full only up to
+//   j0 = (p-1)/2; above that only the cone of coefficients that can still reach the cap is kept:
+//       R_j[K] = (f^j)[cap - K],  K in basis(4(p-1-j)),   R_j[K] = sum_J f[J] * R_{j-1}[K + J].
+//   R_{p-1}[0] is the Fedder coefficient.  (p=5: 165 + 35 + 1 outputs instead of 165 + 455 + 969.)
+//
+// k_power_full (surfaces with height >= 2 only, one CTA per surface, arithmetic mod p^2).
+//   With tau(a) = a^p mod p^2 (Teichmuller representative) and f_T = sum tau(a_J) x^J the chain
+//       f_T^2, f_T^3, ..., f_T^p   (each step: dense product with the <= 35-term f_T, mod p^2)
+//   yields  H = f_T^(p-2), G = f_T^(p-1), Pw = f_T^p  and from them, exactly:
+//       h = H mod p = f^(p-2),   g = G mod p = f^(p-1),
+//       A[I] = ((G[I] - tau(g[I])) mod p^2)/p,   E[J] = ((Pw[J] - [p|J] tau(a_{J/p})) mod p^2)/p  (= Delta_1(f)).
+//   The divisions are exact; a violation raises QFS_ERRBIT_INVARIANT (the reference's
+//   InternalInvariantError, polyring.py:397-398).
+//
+// All arithmetic is integer: residues < p^2 <= 121 in uint8, products accumulated in uint32
+// (35 * 120^2 < 2^32), one reduction per output coefficient.  Lanes/threads own OUTPUT monomials
+// (taken from a precomputed unrank table) and gather over the nonzero terms of f.
 #pragma once
 #include "qfs_shape.cuh"
+
+// unrank table: for k = 1..p the monomials of degree 4k in lex order, packed a1 | a2<<8 | a3<<16;
+// level k starts at unrank_offset(k).
+QFS_HD constexpr int qunrank_offset(int k)
+{
+    int s = 0;
+    for (int j = 1; j < k; ++j) s += qc3(4 * j + 3);
+    return s;
+}
+
+QFS_HD constexpr int qrb_offset(int d)
+{
+    int s = 0;
+    for (int e = 4; e < d; e += 4) s += (e + 1) * (e + 1);
+    return s;
+}
 
 template <int P>
 struct PowerCfg {
     using S = Shape<P>;
-    static constexpr int NT = 128;
-    static constexpr int BUF = S::NE_pad;                      // ping/pong polynomial buffers (uint8)
-    static constexpr int RBDIM = S::dE + 1;                    // row-base table side
-    static constexpr int SMEM = 2 * BUF + 2 * RBDIM * RBDIM;   // + uint16 table
+    static constexpr int J0 = (P - 1) / 2;              // last fully computed level of the Fedder chain
+    static constexpr int FED_WARPS = 8;                 // surfaces per CTA in k_fedder
+    static constexpr int FED_BUF = qround16(qc3(4 * J0 + 3));
+    static constexpr int RB_DEG = 4 * P;                // row-base tables up to this degree
+    static constexpr int FULL_NT = 256;
+    static constexpr int FULL_BUF = S::NE_pad;
+    // row-base tables rb_d for d = 4, 8, ..., RB_DEG; table d starts at rb_offset(d)
+    static QFS_HD constexpr int rb_offset(int d) { return qrb_offset(d); }
+    static constexpr int FED_RB = rb_offset(4 * J0 + 4);       // tables for degrees 4..4*J0
+    static constexpr int FULL_RB = rb_offset(4 * P);           // tables for degrees 4..4(p-1)
+    static constexpr int FED_SMEM = FED_WARPS * 2 * FED_BUF + 2 * FED_RB;
+    static constexpr int FULL_SMEM = 2 * FULL_BUF + 2 * FULL_RB;
 };
 
-template <int P, bool FULL>
-__global__ void __launch_bounds__(PowerCfg<P>::NT)
-k_power(const uint8_t* __restrict__ coeffs, const uint32_t* __restrict__ list, int count,
-        int8_t* __restrict__ heights, uint8_t* __restrict__ fedder_out,
-        uint8_t* __restrict__ g_out, uint8_t* __restrict__ h_out,
-        uint8_t* __restrict__ A_out, uint8_t* __restrict__ E_out, int* __restrict__ err)
+// term list of one quartic: packed j1 | j2<<4 | j3<<8 | j4<<12 | coef<<16, nonzero terms only
+struct TermList {
+    uint32_t t[35];
+    int n;
+};
+
+template <int P>
+__device__ __forceinline__ void fill_rb_tables(uint16_t* rb, int max_deg, int tid, int nt)
+{
+    for (int d = 4; d <= max_deg; d += 4) {
+        uint16_t* t = rb + PowerCfg<P>::rb_offset(d);
+        for (int e = tid; e < (d + 1) * (d + 1); e += nt) {
+            const int a1 = e / (d + 1), a2 = e - a1 * (d + 1);
+            t[e] = (a1 + a2 <= d) ? (uint16_t)qrowbase(d, a1, a2) : (uint16_t)0;
+        }
+    }
+}
+
+// out (degree dout = din+4, all C(dout+3,3) coefficients) = in * f  (mod MOD); threads idx0, idx0+stride, ...
+template <int MOD>
+__device__ __forceinline__ void mul_by_f_full(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, int din,
+                                              const uint16_t* __restrict__ rb_in, const uint32_t* __restrict__ unrank_out,
+                                              const uint32_t* __restrict__ terms, int nf, int idx0, int stride)
+{
+    const int dout = din + 4;
+    const int nout = qc3(dout + 3);
+    for (int o = idx0; o < nout; o += stride) {
+        const uint32_t m = unrank_out[o];
+        const int i1 = m & 255, i2 = (m >> 8) & 255, i3 = m >> 16;
+        uint32_t acc = 0;
+        for (int t = 0; t < nf; ++t) {
+            const uint32_t tm = terms[t];
+            const int a1 = i1 - (int)(tm & 15), a2 = i2 - (int)((tm >> 4) & 15), a3 = i3 - (int)((tm >> 8) & 15);
+            if ((a1 | a2 | a3) >= 0 && a1 + a2 + a3 <= din) acc += (tm >> 16) * in[rb_in[a1 * (din + 1) + a2] + a3];
+        }
+        out[o] = (uint8_t)(acc % (uint32_t)MOD);
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+template <int P>
+__global__ void __launch_bounds__(PowerCfg<P>::FED_WARPS * 32)
+k_fedder(const uint8_t* __restrict__ coeffs, int count, const uint32_t* __restrict__ unrank,
+         int8_t* __restrict__ heights, int* __restrict__ err)
+{
+    using C = PowerCfg<P>;
+    extern __shared__ __align__(16) uint8_t smem[];
+    uint16_t* rb = reinterpret_cast<uint16_t*>(smem + C::FED_WARPS * 2 * C::FED_BUF);
+    __shared__ uint32_t s_terms[C::FED_WARPS][36];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    fill_rb_tables<P>(rb, 4 * C::J0, tid, C::FED_WARPS * 32);
+    __syncthreads();
+
+    const int sid = blockIdx.x * C::FED_WARPS + warp;
+    if (sid >= count) return;
+    const uint8_t* cf = coeffs + (size_t)35 * sid;
+    uint8_t* bufA = smem + (size_t)warp * 2 * C::FED_BUF;
+    uint8_t* bufB = bufA + C::FED_BUF;
+    uint32_t* terms = s_terms[warp];
+
+    // nonzero terms of f via warp ballot; lanes 0..31 hold coefficients 0..31, lanes 0..2 also 32..34
+    const uint32_t* unrank4 = unrank + qunrank_offset(1);
+    int nf = 0;
+    {
+        const uint32_t c0 = cf[lane];
+        const uint32_t c1 = lane < 3 ? cf[32 + lane] : 0;
+        const bool bad = (c0 >= (uint32_t)P) || (c1 >= (uint32_t)P);
+        const unsigned badm = __ballot_sync(0xffffffffu, bad);
+        const unsigned m0 = __ballot_sync(0xffffffffu, c0 != 0 && c0 < (uint32_t)P);
+        const unsigned m1 = __ballot_sync(0xffffffffu, c1 != 0 && c1 < (uint32_t)P);
+        if (lane == 0 && (badm || !(m0 | m1))) atomicOr(err, QFS_ERRBIT_INPUT);
+        bufA[lane] = (uint8_t)(c0 < (uint32_t)P ? c0 : 0);
+        if (lane < 3) bufA[32 + lane] = (uint8_t)(c1 < (uint32_t)P ? c1 : 0);
+        if (m0 >> lane & 1) {
+            const uint32_t mm = unrank4[lane];
+            const uint32_t j1 = mm & 255, j2 = (mm >> 8) & 255, j3 = mm >> 16;
+            terms[__popc(m0 & ((1u << lane) - 1))] = j1 | (j2 << 4) | (j3 << 8) | ((4 - j1 - j2 - j3) << 12) | (c0 << 16);
+        }
+        const int n0 = __popc(m0);
+        if (lane < 3 && (m1 >> lane & 1)) {
+            const uint32_t mm = unrank4[32 + lane];
+            const uint32_t j1 = mm & 255, j2 = (mm >> 8) & 255, j3 = mm >> 16;
+            terms[n0 + __popc(m1 & ((1u << lane) - 1))] = j1 | (j2 << 4) | (j3 << 8) | ((4 - j1 - j2 - j3) << 12) | (c1 << 16);
+        }
+        nf = n0 + __popc(m1);
+    }
+    __syncwarp();
+
+    uint8_t* cur = bufA;
+    uint8_t* nxt = bufB;
+    // full levels f^2 .. f^J0
+#pragma unroll 1
+    for (int j = 2; j <= C::J0; ++j) {
+        mul_by_f_full<P>(cur, nxt, 4 * (j - 1), rb + C::rb_offset(4 * (j - 1)), unrank + qunrank_offset(j), terms, nf, lane, 32);
+        __syncwarp();
+        uint8_t* t = cur; cur = nxt; nxt = t;
+    }
+    // transition level j = J0+1:  R_j[K] = sum_J f[J] * F_J0[cap - K - J],  K in basis(dk), dk = 4(p-2-J0)
+    {
+        constexpr int dk = 4 * (P - 2 - C::J0);
+        constexpr int nk = qc3(dk + 3);
+        constexpr int din = 4 * C::J0;
+        const uint16_t* rbi = rb + C::rb_offset(din);
+        const uint32_t* un = unrank + qunrank_offset(dk / 4);  // unused when dk == 0
+        for (int o = lane; o < nk; o += 32) {
+            int k1 = 0, k2 = 0, k3 = 0;
+            if (dk > 0) { const uint32_t m = un[o]; k1 = m & 255; k2 = (m >> 8) & 255; k3 = m >> 16; }
+            const int k4 = dk - k1 - k2 - k3;
+            uint32_t acc = 0;
+            for (int t = 0; t < nf; ++t) {
+                const uint32_t tm = terms[t];
+                const int a1 = P - 1 - k1 - (int)(tm & 15), a2 = P - 1 - k2 - (int)((tm >> 4) & 15);
+                const int a3 = P - 1 - k3 - (int)((tm >> 8) & 15), a4 = P - 1 - k4 - (int)((tm >> 12) & 15);
+                if ((a1 | a2 | a3 | a4) >= 0) acc += (tm >> 16) * cur[rbi[a1 * (din + 1) + a2] + a3];
+            }
+            nxt[o] = (uint8_t)(acc % (uint32_t)P);
+        }
+        __syncwarp();
+        uint8_t* t = cur; cur = nxt; nxt = t;
+    }
+    // restricted levels j = J0+2 .. p-1:  R_j[K] = sum_J f[J] * R_{j-1}[K + J]
+#pragma unroll 1
+    for (int j = C::J0 + 2; j <= P - 1; ++j) {
+        const int dk = 4 * (P - 1 - j);
+        const int nk = qc3(dk + 3);
+        const int din = dk + 4;
+        const uint16_t* rbi = rb + C::rb_offset(din);
+        const uint32_t* un = unrank + qunrank_offset(dk > 0 ? dk / 4 : 1);
+        for (int o = lane; o < nk; o += 32) {
+            int k1 = 0, k2 = 0, k3 = 0;
+            if (dk > 0) { const uint32_t m = un[o]; k1 = m & 255; k2 = (m >> 8) & 255; k3 = m >> 16; }
+            uint32_t acc = 0;
+            for (int t = 0; t < nf; ++t) {
+                const uint32_t tm = terms[t];
+                acc += (tm >> 16) * cur[rbi[(k1 + (int)(tm & 15)) * (din + 1) + k2 + (int)((tm >> 4) & 15)] + k3 + (int)((tm >> 8) & 15)];
+            }
+            nxt[o] = (uint8_t)(acc % (uint32_t)P);
+        }
+        __syncwarp();
+        uint8_t* t = cur; cur = nxt; nxt = t;
+    }
+    if (lane == 0) heights[sid] = cur[0] ? (int8_t)1 : (int8_t)-1;
+}
+
+// ---------------------------------------------------------------------------------------------
+template <int P>
+__global__ void __launch_bounds__(PowerCfg<P>::FULL_NT)
+k_power_full(const uint8_t* __restrict__ coeffs, const uint32_t* __restrict__ list, int count,
+             const uint32_t* __restrict__ unrank, uint8_t* __restrict__ fedder_out,
+             uint8_t* __restrict__ g_out, uint8_t* __restrict__ h_out,
+             uint8_t* __restrict__ A_out, uint8_t* __restrict__ E_out, int* __restrict__ err)
 {
     using S = Shape<P>;
     using C = PowerCfg<P>;
     constexpr int PSQ = P * P;
+    constexpr int NT = C::FULL_NT;
     extern __shared__ __align__(16) uint8_t smem[];
     uint8_t* bufA = smem;
-    uint8_t* bufB = smem + C::BUF;
-    uint16_t* rbin = reinterpret_cast<uint16_t*>(smem + 2 * C::BUF);
-    __shared__ uint32_t s_terms[35];  // j1 | j2<<4 | j3<<8 | j4<<12 | tau<<16
-    __shared__ uint8_t s_tau35[35];
-    __shared__ uint16_t s_mono[35];   // j1 | j2<<4 | j3<<8
+    uint8_t* bufB = smem + C::FULL_BUF;
+    uint16_t* rb = reinterpret_cast<uint16_t*>(smem + 2 * C::FULL_BUF);
+    __shared__ uint32_t s_terms[36];
+    __shared__ uint8_t s_tau35[36];
     __shared__ int s_nf;
 
     const int slot = blockIdx.x;
     if (slot >= count) return;
     const uint32_t sid = list ? list[slot] : (uint32_t)slot;
     const uint8_t* cf = coeffs + (size_t)35 * sid;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    constexpr int NW = C::NT / 32;
+    const int tid = threadIdx.x;
+    const uint32_t* unrank4 = unrank + qunrank_offset(1);
 
-    if (tid == 0) {
-        int nf = 0, idx = 0, bad = 0, any = 0;
-        for (int j1 = 0; j1 <= 4; ++j1)
-            for (int j2 = 0; j1 + j2 <= 4; ++j2)
-                for (int j3 = 0; j1 + j2 + j3 <= 4; ++j3, ++idx) {
-                    uint32_t c = cf[idx];
-                    if (c >= (uint32_t)P) { bad = 1; c = 0; }
-                    uint32_t t = 1;
-                    for (int i = 0; i < P; ++i) t = t * c % PSQ;  // tau(c) = c^p mod p^2
-                    s_tau35[idx] = (uint8_t)t;
-                    s_mono[idx] = (uint16_t)(j1 | (j2 << 4) | (j3 << 8));
-                    if (c) {
-                        any = 1;
-                        s_terms[nf++] = (uint32_t)j1 | ((uint32_t)j2 << 4) | ((uint32_t)j3 << 8) |
-                                        ((uint32_t)(4 - j1 - j2 - j3) << 12) | (t << 16);
-                    }
-                }
-        s_nf = nf;
-        if (bad || !any) atomicOr(err, QFS_ERRBIT_INPUT);
+    fill_rb_tables<P>(rb, 4 * (P - 1), tid, NT);
+    if (tid < 32) {  // warp 0: Teichmuller lift and compacted term list
+        const int lane = tid;
+        uint32_t c[2] = {cf[lane], lane < 3 ? (uint32_t)cf[32 + lane] : 0u};
+        uint32_t tau[2];
+        bool bad = false;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            if (c[q] >= (uint32_t)P) { bad = true; c[q] = 0; }
+            uint32_t t = 1;
+            for (int i = 0; i < P; ++i) t = t * c[q] % PSQ;  // tau(c) = c^p mod p^2
+            tau[q] = t;
+        }
+        const unsigned badm = __ballot_sync(0xffffffffu, bad);
+        const unsigned m0 = __ballot_sync(0xffffffffu, c[0] != 0);
+        const unsigned m1 = __ballot_sync(0xffffffffu, c[1] != 0);
+        if (lane == 0 && (badm || !(m0 | m1))) atomicOr(err, QFS_ERRBIT_INPUT);
+        s_tau35[lane] = (uint8_t)tau[0];
+        bufA[lane] = (uint8_t)tau[0];
+        if (lane < 3) { s_tau35[32 + lane] = (uint8_t)tau[1]; bufA[32 + lane] = (uint8_t)tau[1]; }
+        const int n0 = __popc(m0);
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const unsigned mq = q ? m1 : m0;
+            if ((q == 0 || lane < 3) && (mq >> lane & 1)) {
+                const uint32_t mm = unrank4[32 * q + lane];
+                const uint32_t j1 = mm & 255, j2 = (mm >> 8) & 255, j3 = mm >> 16;
+                s_terms[(q ? n0 : 0) + __popc(mq & ((1u << lane) - 1))] =
+                    j1 | (j2 << 4) | (j3 << 8) | ((4 - j1 - j2 - j3) << 12) | (tau[q] << 16);
+            }
+        }
+        if (lane == 0) s_nf = n0 + __popc(m1);
     }
     __syncthreads();
     const int nf = s_nf;
-    if (tid < 35) bufA[tid] = s_tau35[tid];
-    __syncthreads();
-
     uint8_t* cur = bufA;
     uint8_t* nxt = bufB;
     const size_t oN = (size_t)slot * S::pitch;
 
-    if (FULL && P == 3) {  // H = f_T itself
+    if (P == 3) {  // H = f_T itself
         if (tid < 35) h_out[(size_t)slot * S::Nh_pad + tid] = (uint8_t)(cur[tid] % P);
     }
-
-    constexpr int KMAX = FULL ? P : P - 2;
 #pragma unroll 1
-    for (int k = 2; k <= KMAX; ++k) {
-        const int din = 4 * (k - 1), dout = 4 * k;
-        for (int e = tid; e < (din + 1) * (din + 1); e += C::NT) {
-            const int a1 = e / (din + 1), a2 = e - a1 * (din + 1);
-            rbin[e] = (a1 + a2 <= din) ? (uint16_t)qrowbase(din, a1, a2) : (uint16_t)0;
-        }
-        __syncthreads();
-        for (int rf = warp; rf < (dout + 1) * (dout + 1); rf += NW) {
-            const int i1 = rf / (dout + 1), i2 = rf - i1 * (dout + 1);
-            const int len = dout - i1 - i2;
-            if (len < 0) continue;
-            const int ob = qrowbase(dout, i1, i2);
-            for (int i3 = lane; i3 <= len; i3 += 32) {
-                uint32_t acc = 0;
-                for (int t = 0; t < nf; ++t) {
-                    const uint32_t tm = s_terms[t];
-                    const int a1 = i1 - (int)(tm & 15), a2 = i2 - (int)((tm >> 4) & 15), a3 = i3 - (int)((tm >> 8) & 15);
-                    if (a1 >= 0 && a2 >= 0 && a3 >= 0 && a1 + a2 + a3 <= din)
-                        acc += (tm >> 16) * cur[rbin[a1 * (din + 1) + a2] + a3];
-                }
-                nxt[ob + i3] = (uint8_t)(acc % PSQ);
-            }
-        }
+    for (int k = 2; k <= P; ++k) {
+        mul_by_f_full<PSQ>(cur, nxt, 4 * (k - 1), rb + C::rb_offset(4 * (k - 1)), unrank + qunrank_offset(k), s_terms, nf, tid, NT);
         __syncthreads();
         { uint8_t* t = cur; cur = nxt; nxt = t; }
-        if (FULL) {
-            if (k == P - 2) {
-                for (int i = tid; i < S::Nh; i += C::NT) h_out[(size_t)slot * S::Nh_pad + i] = (uint8_t)(cur[i] % P);
-            } else if (k == P - 1) {
-                int bad = 0;
-                for (int i = tid; i < S::pitch; i += C::NT) {
-                    uint32_t gi = 0, ai = 0;
-                    if (i < S::N) {
-                        const uint32_t G = cur[i];
-                        gi = G % P;
-                        uint32_t t = 1;
-                        for (int q = 0; q < P; ++q) t = t * gi % PSQ;
-                        const uint32_t num = (G + PSQ - t) % PSQ;
-                        if (num % P) bad = 1;
-                        ai = num / P;
-                    }
-                    g_out[oN + i] = (uint8_t)gi;  // pad bytes are written as zero
-                    A_out[oN + i] = (uint8_t)ai;
+        if (k == P - 2) {
+            for (int i = tid; i < S::Nh; i += NT) h_out[(size_t)slot * S::Nh_pad + i] = (uint8_t)(cur[i] % P);
+        } else if (k == P - 1) {
+            int bad = 0;
+            for (int i = tid; i < S::pitch; i += NT) {
+                uint32_t gi = 0, ai = 0;
+                if (i < S::N) {
+                    const uint32_t G = cur[i];
+                    gi = G % P;
+                    uint32_t t = 1;
+                    for (int q = 0; q < P; ++q) t = t * gi % PSQ;
+                    const uint32_t num = (G + PSQ - t) % PSQ;
+                    if (num % P) bad = 1;
+                    ai = num / P;
                 }
-                if (bad) atomicOr(err, QFS_ERRBIT_INVARIANT);
-                if (fedder_out && tid == 0) fedder_out[slot] = (cur[S::cap] % P) != 0;
-            } else if (k == P) {
-                __syncthreads();
-                if (tid < 35) {  // subtract tau(a_J) at exponent p*J
-                    const int m = s_mono[tid];
-                    const int idx = qrowbase(S::dE, P * (m & 15), P * ((m >> 4) & 15)) + P * ((m >> 8) & 15);
-                    const uint32_t c = cf[tid] < P ? cf[tid] : 0;
-                    cur[idx] = (uint8_t)((cur[idx] + PSQ - (c ? s_tau35[tid] : 0)) % PSQ);
-                }
-                __syncthreads();
-                int bad = 0;
-                for (int i = tid; i < S::NE; i += C::NT) {
-                    const uint32_t v = cur[i];
-                    if (v % P) bad = 1;
-                    E_out[(size_t)slot * S::NE_pad + i] = (uint8_t)(v / P);
-                }
-                if (bad) atomicOr(err, QFS_ERRBIT_INVARIANT);
+                g_out[oN + i] = (uint8_t)gi;  // pad bytes are written as zero
+                A_out[oN + i] = (uint8_t)ai;
             }
-        }
-    }
-
-    if (!FULL) {
-        // Fedder coefficient G[cap] = sum_J f_T[J] * H[(p-1,..,p-1) - J]   (mod p)
-        if (warp == 0) {
-            uint32_t acc = 0;
-            for (int t = lane; t < nf; t += 32) {
-                const uint32_t tm = s_terms[t];
-                const int a1 = P - 1 - (int)(tm & 15), a2 = P - 1 - (int)((tm >> 4) & 15);
-                const int a3 = P - 1 - (int)((tm >> 8) & 15), a4 = P - 1 - (int)((tm >> 12) & 15);
-                if (a1 >= 0 && a2 >= 0 && a3 >= 0 && a4 >= 0)
-                    acc += (tm >> 16) * cur[qrowbase(S::dh, a1, a2) + a3];
+            if (bad) atomicOr(err, QFS_ERRBIT_INVARIANT);
+            if (fedder_out && tid == 0) fedder_out[slot] = (cur[S::cap] % P) != 0;
+        } else if (k == P) {
+            if (tid < 35) {  // subtract tau(a_J) at exponent p*J
+                const uint32_t mm = unrank4[tid];
+                const int idx = qrowbase(S::dE, P * (mm & 255), P * ((mm >> 8) & 255)) + P * (mm >> 16);
+                const uint32_t c = cf[tid] < P ? cf[tid] : 0;
+                cur[idx] = (uint8_t)((cur[idx] + PSQ - (c ? s_tau35[tid] : 0)) % PSQ);
             }
-#pragma unroll
-            for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-            if (lane == 0) heights[sid] = (acc % P) ? (int8_t)1 : (int8_t)-1;
+            __syncthreads();
+            int bad = 0;
+            for (int i = tid; i < S::NE; i += NT) {
+                const uint32_t v = cur[i];
+                if (v % P) bad = 1;
+                E_out[(size_t)slot * S::NE_pad + i] = (uint8_t)(v / P);
+            }
+            if (bad) atomicOr(err, QFS_ERRBIT_INVARIANT);
         }
     }
 }
