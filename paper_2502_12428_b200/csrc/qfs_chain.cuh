@@ -7,7 +7,7 @@
 // dot product is at most N (p-1)^2 <= 12341 * 100 < 2^31, so ONE reduction per row is exact:
 // uint8 x uint8 products are summed four at a time with DP4A into a 32-bit accumulator.
 //
-// Mapping (v1).  Persistent CTAs pull surfaces from a global queue (early exit makes the work per
+// Mapping.  Persistent CTAs pull surfaces from a global queue (early exit makes the work per
 // surface vary from 1 to bound-1 passes over M).  The vector lives in shared memory (ping-pong);
 // each warp owns UNROLL rows at a time, lanes stream 16-byte pieces of those rows from HBM with
 // non-allocating loads, and a warp-shuffle tree finishes each dot product.
@@ -34,7 +34,7 @@ __device__ __forceinline__ uint4 ld_stream16(const uint4* p)
 template <int P>
 __global__ void __launch_bounds__(ChainCfg<P>::NT)
 k_chain(const uint8_t* __restrict__ M_all, const uint8_t* __restrict__ v0_all, const uint32_t* __restrict__ list,
-        int count, int max_steps, uint8_t* __restrict__ trace, int8_t* __restrict__ heights,
+        int count, int start_it, int max_steps, uint8_t* __restrict__ trace, int8_t* __restrict__ heights,
         int8_t* __restrict__ iters, int* __restrict__ queue)
 {
     using S = Shape<P>;
@@ -53,6 +53,17 @@ k_chain(const uint8_t* __restrict__ M_all, const uint8_t* __restrict__ v0_all, c
         const uint8_t* M = M_all + (size_t)slot * ((size_t)S::N * S::pitch);
         uint8_t* va = smem;
         uint8_t* vb = smem + S::pitch;
+        // start_it = 1: v0_all holds v1 = M g from the fused builder (qfs_matrix.cuh); most surfaces are
+        // decided by v1[cap] alone and never touch M here.
+        if (start_it > 0 && (v0_all[(size_t)slot * S::pitch + S::cap] != 0 || max_steps <= start_it)) {
+            if (tid == 0) {
+                const uint32_t sid = list ? list[slot] : (uint32_t)slot;
+                heights[sid] = (int8_t)(v0_all[(size_t)slot * S::pitch + S::cap] != 0 ? start_it + 1 : 0);
+                iters[sid] = (int8_t)start_it;
+            }
+            __syncthreads();
+            continue;
+        }
         {
             const uint4* src = reinterpret_cast<const uint4*>(v0_all + (size_t)slot * S::pitch);
             for (int i = tid; i < NCH; i += C::NT) {
@@ -61,8 +72,8 @@ k_chain(const uint8_t* __restrict__ M_all, const uint8_t* __restrict__ v0_all, c
             }
         }
         __syncthreads();
-        int height = 0, it = 0;
-        for (int step = 1; step <= max_steps; ++step) {
+        int height = 0, it = start_it;
+        for (int step = start_it + 1; step <= max_steps; ++step) {
             for (int row = warp * C::UNROLL; row < S::N; row += NW * C::UNROLL) {
                 uint32_t acc[C::UNROLL];
 #pragma unroll

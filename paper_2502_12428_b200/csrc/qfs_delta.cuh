@@ -17,7 +17,10 @@
 // one LDS.U8 + one IMAD per multiply-add.  Lanes enumerate the (s2, s3) triangle by diagonals
 // through a small table, so all 32 lanes stay busy whatever the triangle size.
 //
-// Output layout: "lex43" (qfs_shape.cuh) -- entry (I1,I2,I3,I4) at rowbase(D,I1,I2) + I4.
+// Output layout: "lex43g" (qfs_shape.cuh) -- entry (I1,I2,I3,I4) at gbase(I1,I2) + I4, every run
+// followed by G guard zeros, ZPAD leading zeros.  The slab staged in shared memory uses the same
+// guard-banded layout (guards stay zero: the flush re-zeroes what it copied), so the guards and
+// the zero pad are (re)written with every surface and need no separate memset.
 #pragma once
 #include "qfs_shape.cuh"
 
@@ -29,10 +32,11 @@ struct DeltaCfg {
     static constexpr int BOX = SB * SB * SB;
     static constexpr int RBDIM = S::dE + 1;
     static constexpr int NTRI = (S::d + 1) * (S::d + 2) / 2;
-    static constexpr int SLAB = qc2(S::D + 2) + 32;
+    static constexpr int SLAB = qc2(S::D + 2) + S::G * (S::D + 1) + 32;
+    static constexpr bool A_IN_SMEM = (P < 11);  // p = 11: the slab needs the room, A is read from HBM
     static constexpr int OFF_E = 0;
     static constexpr int OFF_A = OFF_E + S::NE_pad;
-    static constexpr int OFF_RB = OFF_A + S::pitch;
+    static constexpr int OFF_RB = OFF_A + (A_IN_SMEM ? S::pitch : 0);
     static constexpr int OFF_TRI = OFF_RB + qround16(2 * RBDIM * RBDIM);
     static constexpr int OFF_BOX = OFF_TRI + qround16(2 * NTRI);
     static constexpr int OFF_SLAB = OFF_BOX + qround16(BOX);
@@ -80,10 +84,10 @@ __device__ __forceinline__ void delta_class(const uint8_t* __restrict__ sE, cons
                 for (int t3 = 0; t3 <= K - t1 - t2; ++t3)
                     acc += coef[j++] * hb[-((t1 * SB + t2) * SB + t3)];
         uint32_t a = 0;
-        if (M == 0) a = sA[qrowbase(S::d, s1, s2) + s3];
+        if (M == 0) a = sA[qrowbase(S::d, s1, s2) + s3];  // sA: shared copy, or the surface's A in HBM (p = 11)
         const uint32_t r = (a + (uint32_t)P * 400u - acc) % (uint32_t)P;  // acc <= 35*(p-1)^2 < 400p
         const int I2 = P * s2 + rho2, I4 = P * (ns - kk) + rho4;
-        slab[((I2 * (2 * n + 3 - I2)) >> 1) + I4] = (uint8_t)r;
+        slab[((I2 * (2 * n + 3 - I2)) >> 1) + S::G * I2 + I4] = (uint8_t)r;
     }
 }
 
@@ -96,7 +100,7 @@ k_delta(const uint8_t* __restrict__ h_all, const uint8_t* __restrict__ A_all, co
     using C = DeltaCfg<P>;
     extern __shared__ __align__(16) uint8_t smem[];
     uint8_t* sE = smem + C::OFF_E;
-    uint8_t* sA = smem + C::OFF_A;
+    const uint8_t* sA = C::A_IN_SMEM ? smem + C::OFF_A : A_all + (size_t)blockIdx.x * S::pitch;
     uint16_t* sRB = reinterpret_cast<uint16_t*>(smem + C::OFF_RB);
     uint16_t* sTri = reinterpret_cast<uint16_t*>(smem + C::OFF_TRI);
     uint8_t* sBox = smem + C::OFF_BOX;
@@ -107,13 +111,17 @@ k_delta(const uint8_t* __restrict__ h_all, const uint8_t* __restrict__ A_all, co
     if (slot >= count) return;
     const int tid = threadIdx.x, lane = tid & 31;
     const uint8_t* gh = h_all + (size_t)slot * S::Nh_pad;
-    uint8_t* gd = delta_all + (size_t)slot * S::L_pad;
+    uint8_t* gd = delta_all + (size_t)slot * S::Lg_pad;
 
     {   // stage E, A (16-byte vectors; strides are padded), zero the box, build tables
         const uint4* e4 = reinterpret_cast<const uint4*>(E_all + (size_t)slot * S::NE_pad);
         for (int i = tid; i < S::NE_pad / 16; i += C::NT) reinterpret_cast<uint4*>(sE)[i] = e4[i];
-        const uint4* a4 = reinterpret_cast<const uint4*>(A_all + (size_t)slot * S::pitch);
-        for (int i = tid; i < S::pitch / 16; i += C::NT) reinterpret_cast<uint4*>(sA)[i] = a4[i];
+        if (C::A_IN_SMEM) {
+            const uint4* a4 = reinterpret_cast<const uint4*>(A_all + (size_t)slot * S::pitch);
+            for (int i = tid; i < S::pitch / 16; i += C::NT) reinterpret_cast<uint4*>(smem + C::OFF_A)[i] = a4[i];
+        }
+        for (int i = tid; i < qround16(C::SLAB) / 16; i += C::NT) reinterpret_cast<uint4*>(sSlab)[i] = make_uint4(0, 0, 0, 0);
+        for (int i = tid; i < S::ZPAD / 16; i += C::NT) reinterpret_cast<uint4*>(gd)[i] = make_uint4(0, 0, 0, 0);
         for (int i = tid; i < qround16(C::BOX) / 16; i += C::NT) reinterpret_cast<uint4*>(sBox)[i] = make_uint4(0, 0, 0, 0);
         for (int e = tid; e < C::RBDIM * C::RBDIM; e += C::NT) {
             const int a1 = e / C::RBDIM, a2 = e - a1 * C::RBDIM;
@@ -139,8 +147,8 @@ k_delta(const uint8_t* __restrict__ h_all, const uint8_t* __restrict__ A_all, co
     for (int I1 = 0; I1 <= S::D; ++I1) {
         const int s1 = I1 / P, rho1 = I1 - s1 * P;
         const int n = S::D - I1;
-        const int goff = qc3(S::D + 3) - qc3(n + 3);  // rowbase(D, I1, 0)
-        const int bytes = qc2(n + 2);
+        const int goff = S::gbase(I1, 0);
+        const int bytes = qc2(n + 2) + S::G * (n + 1);  // the slab's runs with their guards
         uint8_t* slab = sSlab + (((size_t)(gd + goff)) & 15);
         if (tid == 0) s_counter = 0;
         __syncthreads();
@@ -165,20 +173,21 @@ k_delta(const uint8_t* __restrict__ h_all, const uint8_t* __restrict__ A_all, co
             uint8_t* dst = gd + goff;
             int head = (16 - (int)(((size_t)dst) & 15)) & 15;
             if (head > bytes) head = bytes;
-            if (tid < head) dst[tid] = slab[tid];
+            if (tid < head) { dst[tid] = slab[tid]; slab[tid] = 0; }
             const int nvec = (bytes - head) >> 4;
-            const uint4* s4 = reinterpret_cast<const uint4*>(slab + head);
+            uint4* s4 = reinterpret_cast<uint4*>(slab + head);
             uint4* d4 = reinterpret_cast<uint4*>(dst + head);
-            for (int i = tid; i < nvec; i += C::NT) d4[i] = s4[i];
+            for (int i = tid; i < nvec; i += C::NT) { d4[i] = s4[i]; s4[i] = make_uint4(0, 0, 0, 0); }
             const int done = head + (nvec << 4);
-            if (tid < bytes - done) dst[done + tid] = slab[done + tid];
+            if (tid < bytes - done) { dst[done + tid] = slab[done + tid]; slab[done + tid] = 0; }
         }
         __syncthreads();
     }
 }
 
-// lex43 <-> lex: reverse every (I1,I2) run (an involution).  Used by the stage taps only.
-template <int P>
+// lex43g <-> lex.  TO_G = true: dense lex input -> guard-banded lex43g output (which must be zero-filled
+// beforehand); TO_G = false: lex43g input -> dense lex output.  Used by the stage taps only.
+template <int P, bool TO_G>
 __global__ void k_delta_flip(const uint8_t* __restrict__ in, size_t in_stride, uint8_t* __restrict__ out,
                              size_t out_stride)
 {
@@ -197,7 +206,8 @@ __global__ void k_delta_flip(const uint8_t* __restrict__ in, size_t in_stride, u
             if (((mid * (2 * n + 3 - mid)) >> 1) <= e) lo = mid; else hi = mid - 1;
         }
         const int rb = (lo * (2 * n + 3 - lo)) >> 1;
-        const int len = n - lo;
-        dst[base + rb + (len - (e - rb))] = src[base + e];
+        const int I4 = (n - lo) - (e - rb);
+        const int gi = S::gbase(I1, lo) + I4;
+        if (TO_G) dst[gi] = src[base + e]; else dst[base + e] = src[gi];
     }
 }

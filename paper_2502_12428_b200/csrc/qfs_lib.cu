@@ -63,7 +63,7 @@ struct qfs_ctx {
     DevBuf colinfo, groups;                         // per-p index tables for the matrix builder
     DevBuf unrank;                                  // per-p unrank tables for the power chain
     DevBuf coeffs, heights, iters, list;            // batch-sized
-    DevBuf g, h, A, E, delta, M;                    // chunk-sized
+    DevBuf g, h, A, E, delta, M, v1;                // chunk-sized
     DevBuf tapA, tapB;                              // staging for the stage taps
     int* h_flags = nullptr;                         // pinned mirror of flags
 };
@@ -150,9 +150,11 @@ int build_tables(qfs_ctx* ctx)
     for (int c1 = 0; c1 <= S::d; ++c1)
         for (int c2 = 0; c1 + c2 <= S::d; ++c2) {
             grp[gidx++] = (uint16_t)(c1 | (c2 << 8));
-            for (int c3 = 0; c1 + c2 + c3 <= S::d; ++c3) col[c++] = (uint32_t)(c1 * (S::d + 1) + c2) | ((uint32_t)c3 << 16);
+            for (int c3 = 0; c1 + c2 + c3 <= S::d; ++c3) col[c++] = (uint32_t)c1 | ((uint32_t)c2 << 8) | ((uint32_t)c3 << 16);
         }
     if (c != S::N || gidx != S::ngroups) return fail(ctx, QFS_EINVAL, "internal: basis enumeration mismatch");
+    // longest row groups first: the builder's CTAs then finish together
+    std::stable_sort(grp.begin(), grp.end(), [](uint16_t a, uint16_t b) { return (a & 255) + (a >> 8) < (b & 255) + (b >> 8); });
     CU(ctx->colinfo.reserve(col.size() * 4));
     CU(ctx->groups.reserve(grp.size() * 2));
     CU(cudaMemcpy(ctx->colinfo.ptr, col.data(), col.size() * 4, cudaMemcpyHostToDevice));
@@ -180,7 +182,7 @@ template <int P>
 size_t per_surface_bytes()
 {
     using S = Shape<P>;
-    return (size_t)S::N * S::pitch + S::L_pad + 2 * (size_t)S::pitch + S::Nh_pad + S::NE_pad;
+    return (size_t)S::N * S::pitch + S::Lg_pad + 3 * (size_t)S::pitch + S::Nh_pad + S::NE_pad;
 }
 
 template <int P>
@@ -191,8 +193,9 @@ int reserve_chunk(qfs_ctx* ctx, size_t cap)
     CU(ctx->A.reserve(cap * S::pitch));
     CU(ctx->h.reserve(cap * S::Nh_pad));
     CU(ctx->E.reserve(cap * S::NE_pad));
-    CU(ctx->delta.reserve(cap * S::L_pad));
+    CU(ctx->delta.reserve(cap * (size_t)S::Lg_pad));
     CU(ctx->M.reserve(cap * (size_t)S::N * S::pitch));
+    CU(ctx->v1.reserve(cap * S::pitch));
     return QFS_OK;
 }
 
@@ -220,26 +223,31 @@ int launch_delta(qfs_ctx* ctx, int count)
 }
 
 template <int P>
-int launch_matrix(qfs_ctx* ctx, int count)
+int launch_matrix(qfs_ctx* ctx, int count, const uint8_t* v0, uint8_t* v1)
 {
     using S = Shape<P>;
-    const unsigned grid = (unsigned)S::ngroups * (unsigned)count;
-    k_matrix<P><<<grid, MatrixCfg<P>::NT, 0, ctx->stream>>>(ctx->delta.as<uint8_t>(), ctx->colinfo.as<uint32_t>(),
-                                                          ctx->groups.as<uint16_t>(), ctx->M.as<uint8_t>(), count);
+    using C = MatrixCfg<P>;
+    const dim3 grid((unsigned)S::ngroups, (unsigned)((count + C::SLICE - 1) / C::SLICE));
+    if (v0)
+        k_matrix<P, true><<<grid, C::NT, 0, ctx->stream>>>(ctx->delta.as<uint8_t>(), ctx->colinfo.as<uint32_t>(),
+                                                          ctx->groups.as<uint16_t>(), ctx->M.as<uint8_t>(), v0, v1, count);
+    else
+        k_matrix<P, false><<<grid, C::NT, 0, ctx->stream>>>(ctx->delta.as<uint8_t>(), ctx->colinfo.as<uint32_t>(),
+                                                           ctx->groups.as<uint16_t>(), ctx->M.as<uint8_t>(), nullptr, nullptr, count);
     ctx->stats.kernel_launches++;
     CU(cudaGetLastError());
     return QFS_OK;
 }
 
 template <int P>
-int launch_chain(qfs_ctx* ctx, const uint8_t* v0, const uint32_t* d_list, int count, int max_steps, uint8_t* trace,
-                 int8_t* heights, int8_t* iters)
+int launch_chain(qfs_ctx* ctx, const uint8_t* v0, const uint32_t* d_list, int count, int start_it, int max_steps,
+                 uint8_t* trace, int8_t* heights, int8_t* iters)
 {
     int* d_queue = ctx->flags.as<int>() + 1;
     CU(cudaMemsetAsync(d_queue, 0, sizeof(int), ctx->stream));
     const int grid = std::min(count, ctx->sm_count * 2);
-    k_chain<P><<<grid, ChainCfg<P>::NT, ChainCfg<P>::SMEM, ctx->stream>>>(ctx->M.as<uint8_t>(), v0, d_list, count, max_steps,
-                                                                        trace, heights, iters, d_queue);
+    k_chain<P><<<grid, ChainCfg<P>::NT, ChainCfg<P>::SMEM, ctx->stream>>>(ctx->M.as<uint8_t>(), v0, d_list, count, start_it,
+                                                                        max_steps, trace, heights, iters, d_queue);
     ctx->stats.kernel_launches++;
     CU(cudaGetLastError());
     return QFS_OK;
@@ -324,7 +332,7 @@ int run_heights(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, int bound, int8_t
         if (!limit) {
             size_t fr = 0, tot = 0;
             CU(cudaMemGetInfo(&fr, &tot));
-            size_t held = ctx->g.cap + ctx->A.cap + ctx->h.cap + ctx->E.cap + ctx->delta.cap + ctx->M.cap;
+            size_t held = ctx->g.cap + ctx->A.cap + ctx->h.cap + ctx->E.cap + ctx->delta.cap + ctx->M.cap + ctx->v1.cap;
             limit = (size_t)((double)(fr + held) * 0.4);
         }
         size_t cap = ctx->chunk_override ? ctx->chunk_override : std::max<size_t>(1, limit / per_surface_bytes<P>());
@@ -346,9 +354,9 @@ int run_heights(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, int bound, int8_t
             CU(cudaEventRecord(ctx->ev[1], ctx->stream));
             if ((rc = launch_delta<P>(ctx, cnt))) return rc;
             CU(cudaEventRecord(ctx->ev[2], ctx->stream));
-            if ((rc = launch_matrix<P>(ctx, cnt))) return rc;
+            if ((rc = launch_matrix<P>(ctx, cnt, ctx->g.as<uint8_t>(), ctx->v1.as<uint8_t>()))) return rc;
             CU(cudaEventRecord(ctx->ev[3], ctx->stream));
-            if ((rc = launch_chain<P>(ctx, ctx->g.as<uint8_t>(), d_list + done, cnt, bound - 1, nullptr, d_heights, d_iters))) return rc;
+            if ((rc = launch_chain<P>(ctx, ctx->v1.as<uint8_t>(), d_list + done, cnt, 1, bound - 1, nullptr, d_heights, d_iters))) return rc;
             CU(cudaEventRecord(ctx->ev[4], ctx->stream));
             CU(cudaEventSynchronize(ctx->ev[4]));
             ctx->stats.ms_power += elapsed(ctx->ev[0], ctx->ev[1]);
@@ -406,7 +414,7 @@ int run_stage_power(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, uint8_t* g, u
     using S = Shape<P>;
     CU(cudaSetDevice(ctx->device));
     CU(cudaMemsetAsync(ctx->flags.ptr, 0, 4 * sizeof(int), ctx->stream));
-    const size_t slice = tap_slice<P>(ctx, B, per_surface_bytes<P>() - (size_t)S::N * S::pitch - S::L_pad + 64);
+    const size_t slice = tap_slice<P>(ctx, B, per_surface_bytes<P>() - (size_t)S::N * S::pitch - S::Lg_pad + 64);
     CU(ctx->tapA.reserve(slice * 35));
     CU(ctx->tapB.reserve(slice));
     for (size_t done = 0; done < B; done += slice) {
@@ -431,7 +439,7 @@ int run_stage_delta(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, uint8_t* delt
     using S = Shape<P>;
     CU(cudaSetDevice(ctx->device));
     CU(cudaMemsetAsync(ctx->flags.ptr, 0, 4 * sizeof(int), ctx->stream));
-    const size_t slice = tap_slice<P>(ctx, B, per_surface_bytes<P>() - (size_t)S::N * S::pitch + S::L_pad);
+    const size_t slice = tap_slice<P>(ctx, B, per_surface_bytes<P>() - (size_t)S::N * S::pitch + S::L);
     CU(ctx->tapA.reserve(slice * 35));
     for (size_t done = 0; done < B; done += slice) {
         const int cnt = (int)std::min(slice, B - done);
@@ -439,16 +447,16 @@ int run_stage_delta(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, uint8_t* delt
         CU(ctx->A.reserve((size_t)cnt * S::pitch));
         CU(ctx->h.reserve((size_t)cnt * S::Nh_pad));
         CU(ctx->E.reserve((size_t)cnt * S::NE_pad));
-        CU(ctx->delta.reserve((size_t)cnt * S::L_pad));
-        CU(ctx->tapB.reserve((size_t)cnt * S::L_pad));
+        CU(ctx->delta.reserve((size_t)cnt * S::Lg_pad));
+        CU(ctx->tapB.reserve((size_t)cnt * S::L));
         CU(cudaMemcpyAsync(ctx->tapA.ptr, coeffs + done * 35, (size_t)cnt * 35, cudaMemcpyDefault, ctx->stream));
         int rc = launch_power_full<P>(ctx, ctx->tapA.as<uint8_t>(), nullptr, cnt, nullptr);
         if (rc) return rc;
         if ((rc = launch_delta<P>(ctx, cnt))) return rc;
         dim3 grid(S::D + 1, cnt);
-        k_delta_flip<P><<<grid, 256, 0, ctx->stream>>>(ctx->delta.as<uint8_t>(), S::L_pad, ctx->tapB.as<uint8_t>(), S::L_pad);
+        k_delta_flip<P, false><<<grid, 256, 0, ctx->stream>>>(ctx->delta.as<uint8_t>(), S::Lg_pad, ctx->tapB.as<uint8_t>(), S::L);
         CU(cudaGetLastError());
-        if ((rc = from_padded(ctx, delta + done * (size_t)S::L, ctx->tapB.ptr, cnt, S::L, S::L_pad))) return rc;
+        CU(cudaMemcpyAsync(delta + done * (size_t)S::L, ctx->tapB.ptr, (size_t)cnt * S::L, cudaMemcpyDefault, ctx->stream));
         CU(cudaStreamSynchronize(ctx->stream));
     }
     return check_device_flags(ctx);
@@ -459,17 +467,19 @@ int run_stage_matrix(qfs_ctx* ctx, const uint8_t* delta, size_t B, uint8_t* M)
 {
     using S = Shape<P>;
     CU(cudaSetDevice(ctx->device));
-    const size_t slice = tap_slice<P>(ctx, B, (size_t)S::N * S::pitch + 2 * (size_t)S::L_pad);
+    const size_t slice = tap_slice<P>(ctx, B, (size_t)S::N * S::pitch + (size_t)S::Lg_pad + S::L);
     for (size_t done = 0; done < B; done += slice) {
         const int cnt = (int)std::min(slice, B - done);
-        int rc = to_padded(ctx, ctx->tapB, delta + done * (size_t)S::L, cnt, S::L, S::L_pad);
-        if (rc) return rc;
-        CU(ctx->delta.reserve((size_t)cnt * S::L_pad));
+        int rc;
+        CU(ctx->tapB.reserve((size_t)cnt * S::L));
+        CU(cudaMemcpyAsync(ctx->tapB.ptr, delta + done * (size_t)S::L, (size_t)cnt * S::L, cudaMemcpyDefault, ctx->stream));
+        CU(ctx->delta.reserve((size_t)cnt * S::Lg_pad));
+        CU(cudaMemsetAsync(ctx->delta.ptr, 0, (size_t)cnt * S::Lg_pad, ctx->stream));
         CU(ctx->M.reserve((size_t)cnt * S::N * S::pitch));
         dim3 grid(S::D + 1, cnt);
-        k_delta_flip<P><<<grid, 256, 0, ctx->stream>>>(ctx->tapB.as<uint8_t>(), S::L_pad, ctx->delta.as<uint8_t>(), S::L_pad);
+        k_delta_flip<P, true><<<grid, 256, 0, ctx->stream>>>(ctx->tapB.as<uint8_t>(), S::L, ctx->delta.as<uint8_t>(), S::Lg_pad);
         CU(cudaGetLastError());
-        if ((rc = launch_matrix<P>(ctx, cnt))) return rc;
+        if ((rc = launch_matrix<P>(ctx, cnt, nullptr, nullptr))) return rc;
         if ((rc = from_padded(ctx, M + done * (size_t)S::N * S::N, ctx->M.ptr, (size_t)cnt * S::N, S::N, S::pitch))) return rc;
         CU(cudaStreamSynchronize(ctx->stream));
     }
@@ -499,7 +509,7 @@ int run_stage_chain(qfs_ctx* ctx, const uint8_t* M, const uint8_t* v0, size_t B,
             CU(cudaMemsetAsync(ctx->tapB.ptr, 0, (size_t)cnt * max_steps * S::N, ctx->stream));
             d_trace = ctx->tapB.as<uint8_t>();
         }
-        if ((rc = launch_chain<P>(ctx, ctx->g.as<uint8_t>(), nullptr, cnt, max_steps, d_trace,
+        if ((rc = launch_chain<P>(ctx, ctx->g.as<uint8_t>(), nullptr, cnt, 0, max_steps, d_trace,
                                   ctx->heights.as<int8_t>() + done, ctx->iters.as<int8_t>() + done)))
             return rc;
         if (d_trace)
@@ -555,7 +565,7 @@ void qfs_destroy(qfs_ctx* ctx)
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     DevBuf* bufs[] = {&ctx->flags, &ctx->colinfo, &ctx->groups, &ctx->unrank, &ctx->coeffs, &ctx->heights, &ctx->iters, &ctx->list,
-                      &ctx->g, &ctx->h, &ctx->A, &ctx->E, &ctx->delta, &ctx->M, &ctx->tapA, &ctx->tapB};
+                      &ctx->g, &ctx->h, &ctx->A, &ctx->E, &ctx->delta, &ctx->M, &ctx->v1, &ctx->tapA, &ctx->tapB};
     for (DevBuf* b : bufs) b->release();
     for (auto& e : ctx->ev) if (e) cudaEventDestroy(e);
     for (auto& e : ctx->ev_total) if (e) cudaEventDestroy(e);

@@ -7,9 +7,15 @@
 //   rowbase(deg,a1,a2) = C(deg+3,3)-C(deg-a1+3,3) + C(deg-a1+2,2)-C(deg-a1-a2+2,2).
 // A "run" is the set of monomials sharing (a1,a2): deg-a1-a2+1 consecutive entries.
 //
-// Internal layout of Delta ("lex43"): same run structure, but inside a run entries are ordered
-// by a4 instead of a3 (the run is stored reversed).  With it every run of an operator-matrix
-// row is a FORWARD contiguous copy of a piece of a Delta run (see qfs_matrix.cuh).
+// Internal layout of Delta ("lex43g"): same run structure, but inside a run entries are ordered
+// by a4 instead of a3 (the run is stored reversed), every run is followed by G = d-p+1 zero
+// bytes ("guard"), and the buffer starts with ZPAD zero bytes:
+//     offset(I1,I2,I3,I4) = gbase(I1,I2) + I4,
+//     gbase(I1,I2) = ZPAD + rowbase(D,I1,I2) + G * runindex(I1,I2),  runindex = I1(D+1) - I1(I1-1)/2 + I2.
+// With it every run of an operator-matrix row is a FORWARD contiguous copy of a piece of a Delta
+// run, out-of-range exponents (I3 < 0 or I4 < 0, at most G steps outside the run) land on guard
+// zeros, and columns that can never match read the leading zero pad: the matrix builder needs
+// no validity predicates at all (see qfs_matrix.cuh).
 #pragma once
 #include <stdint.h>
 
@@ -45,6 +51,14 @@ struct Shape {
     static constexpr int L_pad = qround16(L);
     static constexpr int cap = qrowbase(d, P - 1, P - 1) + P - 1;
     static constexpr int ngroups = (d + 1) * (d + 2) / 2;  // (r1,r2) row groups of M
+    // guard-banded Delta layout (lex43g)
+    static constexpr int G = d - P + 1;                    // farthest out-of-run read of the builder
+    static constexpr int ZPAD = qround16(P * d + 1);       // leading zeros: covers offset p*(R-r3) <= p*d
+    static constexpr int nruns = (D + 1) * (D + 2) / 2;
+    static constexpr int Lg = ZPAD + L + G * nruns;
+    static constexpr int Lg_pad = qround16(Lg);
+    static QFS_HD constexpr int runindex(int I1, int I2) { return I1 * (D + 1) - I1 * (I1 - 1) / 2 + I2; }
+    static QFS_HD constexpr int gbase(int I1, int I2) { return ZPAD + qrowbase(D, I1, I2) + G * runindex(I1, I2); }
 };
 
 // error bits raised by kernels into the context's device flag word
