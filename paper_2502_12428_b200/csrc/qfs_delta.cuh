@@ -3,19 +3,25 @@
 // Replaces delta1(g) (polyring.py:335-401) and its inner power_mod_small (nttpower.py:447-507):
 // instead of raising the N-term g to the p-th power (an NTT of length 2^21..2^27 over 3..6 helper
 // primes in the reference) the carry is assembled from the pieces stage 1 produced,
-//     Delta[p*s + rho] = [rho = 0] * A[s]  -  sum_{t >= 0, |t| = 4 - m}  E[rho + p*t] * h[s - t]      (mod p)
-// for every residue class rho in [0,p)^4 with |rho| = m*p (m = 0..3) and every s of degree 4(p-1)-m
-// (DESIGN.md section 3 derives it; tests/model_factorized.py restates it in numpy).
-// That is C(4p+3,3) * C(4p-5,3) exact integer multiply-adds per surface (0.8 M at p=5, 8 M at p=7,
+//     Delta = phi(A) - phi(h) * E   (mod p),   phi: x_i -> x_i^p,
+// (DESIGN.md section 3 derives it; tests/model_factorized.py restates it in numpy).  Dehomogenised
+// (x4 = 1) this is a plain product of 3-variable polynomials: writing an exponent of Delta as
+// I = p*s + rho with 0 <= rho_k < p (k = 1..3),
+//     Delta[p*s + rho] = [rho = 0] * A[s]  -  sum_{t in T}  E[rho + p*t] * h[s - t],
+// where T = {t in N^3 : t1+t2+t3 <= 4} has 35 elements and E, h are zero outside their supports.
+// That is C(4p+3,3) * C(4p-5,3) useful integer multiply-adds per surface (0.8 M at p=5, 8 M at p=7,
 // 148 M at p=11) with no FFT and no floating point.
 //
-// Mapping.  h sits in shared memory as a zero-padded (dh+9)^3 box so that "s - t" is one subtraction
-// of a compile-time offset and out-of-range reads are zeros.  The output is produced slab by slab
-// (slab = all exponents with a fixed I1), staged in shared memory and written to HBM with 16-byte
-// coalesced stores.  Inside a slab each warp takes one class (rho2, rho3) at a time: the <= 35 tap
-// coefficients E[rho + p t] are then warp-uniform registers and the inner loop is
-// one LDS.U8 + one IMAD per multiply-add.  Lanes enumerate the (s2, s3) triangle by diagonals
-// through a small table, so all 32 lanes stay busy whatever the triangle size.
+// Mapping.  The 35 values h[s - t] depend on the point s only, the 35 coefficients E[rho + p*t] on
+// the residue class rho only.  Both are packed four taps to a 32-bit word (taps ordered by
+// t1+t2+t3, so a class whose rho leaves room for |t| <= k only needs a prefix of 1/3/5/9 words):
+//   * sEc  [class][9 words]   -- built once per surface from E,
+//   * sHp  [9 words][point]   -- built once per s1-layer from a zero-padded box copy of h,
+// and one output is  (A - sum_w dp4a(sEc[class][w], sHp[w][point])) mod p : one broadcast LDS.32 and
+// one DP4A per four multiply-adds.  The output is produced slab by slab (slab = all exponents with
+// a fixed I1 = p*s1 + rho1), staged in shared memory in the final guard-banded layout and written
+// to HBM with 16-byte coalesced stores.  Inside a slab the work items are (rho2, point (s2,s3)),
+// P*T(s1) of them, dealt to threads with rho2 (hence the class) uniform per warp.
 //
 // Output layout: "lex43g" (qfs_shape.cuh) -- entry (I1,I2,I3,I4) at gbase(I1,I2) + I4, every run
 // followed by G guard zeros, ZPAD leading zeros.  The slab staged in shared memory uses the same
@@ -27,68 +33,33 @@
 template <int P>
 struct DeltaCfg {
     using S = Shape<P>;
-    static constexpr int NT = (P >= 11) ? 512 : 256;
-    static constexpr int SB = S::dh + 9;  // box side: 4 zeros below, 4 above
-    static constexpr int BOX = SB * SB * SB;
-    static constexpr int RBDIM = S::dE + 1;
-    static constexpr int NTRI = (S::d + 1) * (S::d + 2) / 2;
+    static constexpr int NT = (P >= 11) ? 512 : (P >= 7 ? 256 : (P >= 5 ? 128 : 64));
+    static constexpr bool USE_BOX = (P < 11);  // p = 11: no room for the box; h is read with bounds checks
+    static constexpr bool A_IN_SMEM = (P < 11);
+    static constexpr int SB = S::dh + 9;       // box side: 4 zeros below, 4 above
+    static constexpr int BOX = USE_BOX ? SB * SB * SB : 0;
+    static constexpr int NTAP = 35, NWORD = 9;
+    static constexpr int NCLS = P * P * P;
+    static constexpr int TMAX = (S::d + 1) * (S::d + 2) / 2;  // points (s2,s3) of the layer s1 = 0
+    static constexpr int TPAD = (TMAX + 31) & ~31;
+    static constexpr int RBH = (S::dh + 1) * (S::dh + 1);     // row bases of basis(dh) (bounds-checked path)
     static constexpr int SLAB = qc2(S::D + 2) + S::G * (S::D + 1) + 32;
-    static constexpr bool A_IN_SMEM = (P < 11);  // p = 11: the slab needs the room, A is read from HBM
-    static constexpr int OFF_E = 0;
-    static constexpr int OFF_A = OFF_E + S::NE_pad;
-    static constexpr int OFF_RB = OFF_A + (A_IN_SMEM ? S::pitch : 0);
-    static constexpr int OFF_TRI = OFF_RB + qround16(2 * RBDIM * RBDIM);
-    static constexpr int OFF_BOX = OFF_TRI + qround16(2 * NTRI);
-    static constexpr int OFF_SLAB = OFF_BOX + qround16(BOX);
+    static constexpr int OFF_EC = 0;                                   // uint32 [NCLS][9]
+    static constexpr int OFF_HP = OFF_EC + qround16(NCLS * NWORD * 4);  // uint32 [9][TPAD]
+    static constexpr int OFF_A = OFF_HP + NWORD * TPAD * 4;
+    static constexpr int OFF_TRI = OFF_A + (A_IN_SMEM ? S::pitch : 0);  // uint16 [TMAX]
+    static constexpr int OFF_H = OFF_TRI + qround16(2 * TMAX);          // box, or lex h + row-base table
+    static constexpr int OFF_SLAB = OFF_H + (USE_BOX ? qround16(BOX) : qround16(S::Nh_pad + 2 * RBH));
     static constexpr int SMEM = OFF_SLAB + qround16(SLAB);
 };
 
-// One class (rho; m = M) of one slab, executed by one warp.
-template <int P, int M>
-__device__ __forceinline__ void delta_class(const uint8_t* __restrict__ sE, const uint8_t* __restrict__ sA,
-                                            const uint16_t* __restrict__ sRB, const uint16_t* __restrict__ sTri,
-                                            const uint8_t* __restrict__ sBox, uint8_t* __restrict__ slab,
-                                            int s1, int rho1, int rho2, int rho3, int rho4, int n, int lane)
+template <int NW>
+__device__ __forceinline__ uint32_t delta_dot(const uint32_t* __restrict__ ec, const uint32_t (&hp)[9])
 {
-    using S = Shape<P>;
-    using C = DeltaCfg<P>;
-    constexpr int K = 4 - M;                       // degree of the tap polynomial E_rho
-    constexpr int CNT = (K + 1) * (K + 2) * (K + 3) / 6;
-    constexpr int SB = C::SB;
-    const int ns = (S::d - M) - s1;                // (s2,s3,s4) has degree ns
-    if (ns < 0) return;
-
-    uint32_t coef[CNT];
-    {
-        int j = 0;
+    uint32_t acc = 0;
 #pragma unroll
-        for (int t1 = 0; t1 <= K; ++t1)
-#pragma unroll
-            for (int t2 = 0; t2 <= K - t1; ++t2)
-#pragma unroll
-                for (int t3 = 0; t3 <= K - t1 - t2; ++t3)
-                    coef[j++] = sE[sRB[(rho1 + P * t1) * C::RBDIM + rho2 + P * t2] + rho3 + P * t3];
-    }
-    const int ntri = (ns + 1) * (ns + 2) / 2;
-    for (int q = lane; q < ntri; q += 32) {
-        const uint32_t e = sTri[q];
-        const int kk = e & 255, s2 = e >> 8, s3 = kk - s2;
-        const uint8_t* hb = sBox + ((s1 + 4) * SB + (s2 + 4)) * SB + (s3 + 4);
-        uint32_t acc = 0;
-        int j = 0;
-#pragma unroll
-        for (int t1 = 0; t1 <= K; ++t1)
-#pragma unroll
-            for (int t2 = 0; t2 <= K - t1; ++t2)
-#pragma unroll
-                for (int t3 = 0; t3 <= K - t1 - t2; ++t3)
-                    acc += coef[j++] * hb[-((t1 * SB + t2) * SB + t3)];
-        uint32_t a = 0;
-        if (M == 0) a = sA[qrowbase(S::d, s1, s2) + s3];  // sA: shared copy, or the surface's A in HBM (p = 11)
-        const uint32_t r = (a + (uint32_t)P * 400u - acc) % (uint32_t)P;  // acc <= 35*(p-1)^2 < 400p
-        const int I2 = P * s2 + rho2, I4 = P * (ns - kk) + rho4;
-        slab[((I2 * (2 * n + 3 - I2)) >> 1) + S::G * I2 + I4] = (uint8_t)r;
-    }
+    for (int w = 0; w < NW; ++w) acc = __dp4a(ec[w], hp[w], acc);
+    return acc;
 }
 
 template <int P>
@@ -99,73 +70,143 @@ k_delta(const uint8_t* __restrict__ h_all, const uint8_t* __restrict__ A_all, co
     using S = Shape<P>;
     using C = DeltaCfg<P>;
     extern __shared__ __align__(16) uint8_t smem[];
-    uint8_t* sE = smem + C::OFF_E;
-    const uint8_t* sA = C::A_IN_SMEM ? smem + C::OFF_A : A_all + (size_t)blockIdx.x * S::pitch;
-    uint16_t* sRB = reinterpret_cast<uint16_t*>(smem + C::OFF_RB);
+    uint32_t* sEc = reinterpret_cast<uint32_t*>(smem + C::OFF_EC);
+    uint32_t* sHp = reinterpret_cast<uint32_t*>(smem + C::OFF_HP);
     uint16_t* sTri = reinterpret_cast<uint16_t*>(smem + C::OFF_TRI);
-    uint8_t* sBox = smem + C::OFF_BOX;
+    uint8_t* sH = smem + C::OFF_H;
     uint8_t* sSlab = smem + C::OFF_SLAB;
-    __shared__ int s_counter;
 
     const int slot = blockIdx.x;
     if (slot >= count) return;
-    const int tid = threadIdx.x, lane = tid & 31;
+    const int tid = threadIdx.x;
     const uint8_t* gh = h_all + (size_t)slot * S::Nh_pad;
+    const uint8_t* gE = E_all + (size_t)slot * S::NE_pad;
+    const uint8_t* sA = C::A_IN_SMEM ? smem + C::OFF_A : A_all + (size_t)slot * S::pitch;
     uint8_t* gd = delta_all + (size_t)slot * S::Lg_pad;
 
-    {   // stage E, A (16-byte vectors; strides are padded), zero the box, build tables
-        const uint4* e4 = reinterpret_cast<const uint4*>(E_all + (size_t)slot * S::NE_pad);
-        for (int i = tid; i < S::NE_pad / 16; i += C::NT) reinterpret_cast<uint4*>(sE)[i] = e4[i];
-        if (C::A_IN_SMEM) {
-            const uint4* a4 = reinterpret_cast<const uint4*>(A_all + (size_t)slot * S::pitch);
-            for (int i = tid; i < S::pitch / 16; i += C::NT) reinterpret_cast<uint4*>(smem + C::OFF_A)[i] = a4[i];
-        }
-        for (int i = tid; i < qround16(C::SLAB) / 16; i += C::NT) reinterpret_cast<uint4*>(sSlab)[i] = make_uint4(0, 0, 0, 0);
-        for (int i = tid; i < S::ZPAD / 16; i += C::NT) reinterpret_cast<uint4*>(gd)[i] = make_uint4(0, 0, 0, 0);
-        for (int i = tid; i < qround16(C::BOX) / 16; i += C::NT) reinterpret_cast<uint4*>(sBox)[i] = make_uint4(0, 0, 0, 0);
-        for (int e = tid; e < C::RBDIM * C::RBDIM; e += C::NT) {
-            const int a1 = e / C::RBDIM, a2 = e - a1 * C::RBDIM;
-            sRB[e] = (a1 + a2 <= S::dE) ? (uint16_t)qrowbase(S::dE, a1, a2) : (uint16_t)0;
-        }
-        for (int e = tid; e < (S::d + 1) * (S::d + 1); e += C::NT) {
-            const int kk = e / (S::d + 1), s2 = e - kk * (S::d + 1);
-            if (s2 <= kk) sTri[kk * (kk + 1) / 2 + s2] = (uint16_t)(kk | (s2 << 8));
+    // ---- per-surface setup -------------------------------------------------------------------
+    if (C::A_IN_SMEM) {
+        const uint4* a4 = reinterpret_cast<const uint4*>(A_all + (size_t)slot * S::pitch);
+        for (int i = tid; i < S::pitch / 16; i += C::NT) reinterpret_cast<uint4*>(smem + C::OFF_A)[i] = a4[i];
+    }
+    for (int i = tid; i < qround16(C::SLAB) / 16; i += C::NT) reinterpret_cast<uint4*>(sSlab)[i] = make_uint4(0, 0, 0, 0);
+    for (int i = tid; i < S::ZPAD / 16; i += C::NT) reinterpret_cast<uint4*>(gd)[i] = make_uint4(0, 0, 0, 0);
+    for (int e = tid; e < (S::d + 1) * (S::d + 1); e += C::NT) {  // points of a layer by diagonals kk = s2+s3
+        const int kk = e / (S::d + 1), s2 = e - kk * (S::d + 1);
+        if (s2 <= kk) sTri[kk * (kk + 1) / 2 + s2] = (uint16_t)(kk | (s2 << 8));
+    }
+    if (C::USE_BOX) {
+        for (int i = tid; i < qround16(C::BOX) / 16; i += C::NT) reinterpret_cast<uint4*>(sH)[i] = make_uint4(0, 0, 0, 0);
+    } else {
+        for (int i = tid; i < S::Nh_pad / 16; i += C::NT)
+            reinterpret_cast<uint4*>(sH)[i] = reinterpret_cast<const uint4*>(gh)[i];
+        uint16_t* rbh = reinterpret_cast<uint16_t*>(sH + S::Nh_pad);
+        for (int e = tid; e < C::RBH; e += C::NT) {
+            const int u1 = e / (S::dh + 1), u2 = e - u1 * (S::dh + 1);
+            rbh[e] = (u1 + u2 <= S::dh) ? (uint16_t)qrowbase(S::dh, u1, u2) : (uint16_t)0;
         }
     }
+    // class table: sEc[c][w] byte b = E[rho + p*t_j], j = 4w+b, taps ordered by |t| then lex; 0 outside deg 4p
+    for (int e = tid; e < C::NCLS * C::NWORD; e += C::NT) {
+        const int c = e / C::NWORD, w = e - c * C::NWORD;
+        const int rho1 = c / (P * P), rho2 = (c / P) % P, rho3 = c % P;
+        uint32_t word = 0;
+        int j = 0;
+#pragma unroll
+        for (int k = 0; k <= 4; ++k)
+#pragma unroll
+            for (int t1 = 0; t1 <= k; ++t1)
+#pragma unroll
+                for (int t2 = 0; t2 <= k - t1; ++t2) {
+                    const int t3 = k - t1 - t2;
+                    if ((j >> 2) == w) {
+                        const int J1 = rho1 + P * t1, J2 = rho2 + P * t2, J3 = rho3 + P * t3;
+                        if (J1 + J2 + J3 <= S::dE) word |= (uint32_t)gE[qrowbase(S::dE, J1, J2) + J3] << (8 * (j & 3));
+                    }
+                    ++j;
+                }
+        sEc[e] = word;
+    }
     __syncthreads();
-    for (int e = tid; e < (S::dh + 1) * (S::dh + 1); e += C::NT) {
-        const int u1 = e / (S::dh + 1), u2 = e - u1 * (S::dh + 1);
-        const int len = S::dh - u1 - u2;
-        if (len < 0) continue;
-        const uint8_t* src = gh + qrowbase(S::dh, u1, u2);
-        uint8_t* dst = sBox + ((u1 + 4) * C::SB + (u2 + 4)) * C::SB + 4;
-        for (int u3 = 0; u3 <= len; ++u3) dst[u3] = src[u3];
+    if (C::USE_BOX) {
+        for (int e = tid; e < (S::dh + 1) * (S::dh + 1); e += C::NT) {
+            const int u1 = e / (S::dh + 1), u2 = e - u1 * (S::dh + 1);
+            const int len = S::dh - u1 - u2;
+            if (len < 0) continue;
+            const uint8_t* src = gh + qrowbase(S::dh, u1, u2);
+            uint8_t* dst = sH + ((u1 + 4) * C::SB + (u2 + 4)) * C::SB + 4;
+            for (int u3 = 0; u3 <= len; ++u3) dst[u3] = src[u3];
+        }
     }
     __syncthreads();
 
+    // ---- slabs ---------------------------------------------------------------------------------
 #pragma unroll 1
     for (int I1 = 0; I1 <= S::D; ++I1) {
         const int s1 = I1 / P, rho1 = I1 - s1 * P;
         const int n = S::D - I1;
+        const int ns = S::d - s1;
+        const int T = (ns + 1) * (ns + 2) / 2;
+        if (rho1 == 0) {
+            // packed h neighbourhoods of the layer's points: sHp[w][q] byte b = h[s - t_j], j = 4w+b
+            for (int q = tid; q < T; q += C::NT) {
+                const uint32_t e = sTri[q];
+                const int kk = e & 255, s2 = e >> 8, s3 = kk - s2;
+                uint32_t word = 0;
+                int j = 0;
+#pragma unroll
+                for (int k = 0; k <= 4; ++k)
+#pragma unroll
+                    for (int t1 = 0; t1 <= k; ++t1)
+#pragma unroll
+                        for (int t2 = 0; t2 <= k - t1; ++t2) {
+                            const int t3 = k - t1 - t2;
+                            uint32_t hv;
+                            if (C::USE_BOX) {
+                                hv = sH[((s1 + 4 - t1) * C::SB + (s2 + 4 - t2)) * C::SB + (s3 + 4 - t3)];
+                            } else {
+                                const int u1 = s1 - t1, u2 = s2 - t2, u3 = s3 - t3;
+                                hv = 0;
+                                if (u1 >= 0 && u2 >= 0 && u3 >= 0 && u1 + u2 + u3 <= S::dh)
+                                    hv = sH[reinterpret_cast<const uint16_t*>(sH + S::Nh_pad)[u1 * (S::dh + 1) + u2] + u3];
+                            }
+                            word |= hv << (8 * (j & 3));
+                            if ((j & 3) == 3) { sHp[(j >> 2) * C::TPAD + q] = word; word = 0; }
+                            ++j;
+                        }
+                sHp[8 * C::TPAD + q] = word;  // taps 32..34
+            }
+            __syncthreads();
+        }
         const int goff = S::gbase(I1, 0);
         const int bytes = qc2(n + 2) + S::G * (n + 1);  // the slab's runs with their guards
         uint8_t* slab = sSlab + (((size_t)(gd + goff)) & 15);
-        if (tid == 0) s_counter = 0;
-        __syncthreads();
-        while (true) {
-            int cls = 0;
-            if (lane == 0) cls = atomicAdd(&s_counter, 1);
-            cls = __shfl_sync(0xffffffffu, cls, 0);
-            if (cls >= P * P) break;
-            const int rho2 = cls / P, rho3 = cls - rho2 * P;
-            const int rs = rho1 + rho2 + rho3;
-            const int rho4 = (P - rs % P) % P;
-            const int m = (rs + rho4) / P;
-            switch (m) {
-                case 0: delta_class<P, 0>(sE, sA, sRB, sTri, sBox, slab, s1, rho1, rho2, rho3, rho4, n, lane); break;
-                case 1: delta_class<P, 1>(sE, sA, sRB, sTri, sBox, slab, s1, rho1, rho2, rho3, rho4, n, lane); break;
-                case 2: delta_class<P, 2>(sE, sA, sRB, sTri, sBox, slab, s1, rho1, rho2, rho3, rho4, n, lane); break;
-                default: delta_class<P, 3>(sE, sA, sRB, sTri, sBox, slab, s1, rho1, rho2, rho3, rho4, n, lane); break;
+        const float invT = 1.0f / (float)T;
+        for (int i = tid; i < P * T; i += C::NT) {
+            const int rho2 = (int)(((float)i + 0.5f) * invT);
+            const int q = i - rho2 * T;
+            const uint32_t e = sTri[q];
+            const int kk = e & 255, s2 = e >> 8, s3 = kk - s2;
+            const int I2 = P * s2 + rho2;
+            const int n2 = n - I2;
+            if (n2 < 0) continue;
+            uint32_t hp[9];
+#pragma unroll
+            for (int w = 0; w < 9; ++w) hp[w] = sHp[w * C::TPAD + q];
+            uint8_t* out = slab + ((I2 * (2 * n + 3 - I2)) >> 1) + S::G * I2 + (n2 - P * s3);  // position of rho3 = 0
+            const uint32_t* ec = sEc + ((rho1 * P + rho2) * P) * C::NWORD;
+            const int rs12 = rho1 + rho2;
+#pragma unroll
+            for (int rho3 = 0; rho3 < P; ++rho3) {
+                const int rs = rs12 + rho3;
+                uint32_t acc;
+                if (rs > 2 * P) acc = delta_dot<1>(ec + rho3 * C::NWORD, hp);
+                else if (rs > P) acc = delta_dot<3>(ec + rho3 * C::NWORD, hp);
+                else if (rs > 0) acc = delta_dot<5>(ec + rho3 * C::NWORD, hp);
+                else acc = delta_dot<9>(ec + rho3 * C::NWORD, hp) + (uint32_t)P * 400u - (uint32_t)sA[qrowbase(S::d, s1, s2) + s3];
+                // acc <= 35 (p-1)^2 < 400 p; for rho = 0 the line above turned it into 400p + acc - A
+                const uint32_t r = ((uint32_t)P * 800u - acc) % (uint32_t)P;
+                if (P * s3 + rho3 <= n2) out[-rho3] = (uint8_t)r;
             }
         }
         __syncthreads();
