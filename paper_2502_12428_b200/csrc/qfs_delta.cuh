@@ -50,16 +50,25 @@ struct DeltaCfg {
     static constexpr int OFF_TRI = OFF_A + (A_IN_SMEM ? S::pitch : 0);  // uint16 [TMAX]
     static constexpr int OFF_H = OFF_TRI + qround16(2 * TMAX);          // box, or lex h + row-base table
     static constexpr int OFF_SLAB = OFF_H + (USE_BOX ? qround16(BOX) : qround16(S::Nh_pad + 2 * RBH));
-    static constexpr int SMEM = OFF_SLAB + qround16(SLAB);
+    static constexpr int SMEM = OFF_SLAB + qround16(SLAB) + 16;  // + sink bytes
 };
 
-template <int NW>
-__device__ __forceinline__ uint32_t delta_dot(const uint32_t* __restrict__ ec, const uint32_t (&hp)[9])
+// acc[rho3] = sum over the first NW tap words of class (rho1,rho2,rho3), for rho3 = 0..P-1
+template <int P, int NW>
+__device__ __forceinline__ void delta_classes(const uint32_t* __restrict__ ec, const uint32_t* __restrict__ hpq,
+                                              uint32_t (&acc)[P])
 {
-    uint32_t acc = 0;
+    using C = DeltaCfg<P>;
+    uint32_t hp[NW];
 #pragma unroll
-    for (int w = 0; w < NW; ++w) acc = __dp4a(ec[w], hp[w], acc);
-    return acc;
+    for (int w = 0; w < NW; ++w) hp[w] = hpq[w * C::TPAD];
+#pragma unroll
+    for (int rho3 = 0; rho3 < P; ++rho3) {
+        uint32_t a = 0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) a = __dp4a(ec[rho3 * C::NWORD + w], hp[w], a);
+        acc[rho3] = a;
+    }
 }
 
 template <int P>
@@ -106,7 +115,7 @@ k_delta(const uint8_t* __restrict__ h_all, const uint8_t* __restrict__ A_all, co
             rbh[e] = (u1 + u2 <= S::dh) ? (uint16_t)qrowbase(S::dh, u1, u2) : (uint16_t)0;
         }
     }
-    // class table: sEc[c][w] byte b = E[rho + p*t_j], j = 4w+b, taps ordered by |t| then lex; 0 outside deg 4p
+    // class table: sEc[c][w] byte b = -E[rho + p*t_j] mod p, j = 4w+b, taps ordered by |t| then lex; 0 outside deg 4p
     for (int e = tid; e < C::NCLS * C::NWORD; e += C::NT) {
         const int c = e / C::NWORD, w = e - c * C::NWORD;
         const int rho1 = c / (P * P), rho2 = (c / P) % P, rho3 = c % P;
@@ -121,7 +130,10 @@ k_delta(const uint8_t* __restrict__ h_all, const uint8_t* __restrict__ A_all, co
                     const int t3 = k - t1 - t2;
                     if ((j >> 2) == w) {
                         const int J1 = rho1 + P * t1, J2 = rho2 + P * t2, J3 = rho3 + P * t3;
-                        if (J1 + J2 + J3 <= S::dE) word |= (uint32_t)gE[qrowbase(S::dE, J1, J2) + J3] << (8 * (j & 3));
+                        if (J1 + J2 + J3 <= S::dE) {
+                            const uint32_t ev = gE[qrowbase(S::dE, J1, J2) + J3];
+                            word |= (ev ? (uint32_t)P - ev : 0u) << (8 * (j & 3));  // -E mod p: sums stay non-negative
+                        }
                     }
                     ++j;
                 }
@@ -181,6 +193,7 @@ k_delta(const uint8_t* __restrict__ h_all, const uint8_t* __restrict__ A_all, co
         const int goff = S::gbase(I1, 0);
         const int bytes = qc2(n + 2) + S::G * (n + 1);  // the slab's runs with their guards
         uint8_t* slab = sSlab + (((size_t)(gd + goff)) & 15);
+        uint8_t* dummy = sSlab + qround16(C::SLAB) + (tid & 15);  // sink for the stores of non-exponents
         const float invT = 1.0f / (float)T;
         for (int i = tid; i < P * T; i += C::NT) {
             const int rho2 = (int)(((float)i + 0.5f) * invT);
@@ -190,23 +203,29 @@ k_delta(const uint8_t* __restrict__ h_all, const uint8_t* __restrict__ A_all, co
             const int I2 = P * s2 + rho2;
             const int n2 = n - I2;
             if (n2 < 0) continue;
-            uint32_t hp[9];
-#pragma unroll
-            for (int w = 0; w < 9; ++w) hp[w] = sHp[w * C::TPAD + q];
             uint8_t* out = slab + ((I2 * (2 * n + 3 - I2)) >> 1) + S::G * I2 + (n2 - P * s3);  // position of rho3 = 0
             const uint32_t* ec = sEc + ((rho1 * P + rho2) * P) * C::NWORD;
+            const uint32_t* hpq = sHp + q;
             const int rs12 = rho1 + rho2;
+            // |rho| = rs12 + rho3 leaves room for |t| <= 4 - ceil(|rho|/p): a prefix of 9/5/3/1 tap words.  The
+            // prefix length is taken from rs12 alone (uniform over rho3; the extra words hold zeros).
+            uint32_t acc[P];
+            if (rs12 > 2 * P) delta_classes<P, 1>(ec, hpq, acc);
+            else if (rs12 > P) delta_classes<P, 3>(ec, hpq, acc);
+            else delta_classes<P, 5>(ec, hpq, acc);
+            if (rs12 == 0) {  // class rho = 0: all 35 taps, plus the phi(A) term
+                uint32_t a = acc[0];
+#pragma unroll
+                for (int w = 5; w < 9; ++w) a = __dp4a(ec[w], hpq[w * C::TPAD], a);
+                acc[0] = a + (uint32_t)sA[qrowbase(S::d, s1, s2) + s3];
+            }
+            const int room = n2 - P * s3;  // rho3 <= room are real exponents (I4 >= 0)
 #pragma unroll
             for (int rho3 = 0; rho3 < P; ++rho3) {
-                const int rs = rs12 + rho3;
-                uint32_t acc;
-                if (rs > 2 * P) acc = delta_dot<1>(ec + rho3 * C::NWORD, hp);
-                else if (rs > P) acc = delta_dot<3>(ec + rho3 * C::NWORD, hp);
-                else if (rs > 0) acc = delta_dot<5>(ec + rho3 * C::NWORD, hp);
-                else acc = delta_dot<9>(ec + rho3 * C::NWORD, hp) + (uint32_t)P * 400u - (uint32_t)sA[qrowbase(S::d, s1, s2) + s3];
-                // acc <= 35 (p-1)^2 < 400 p; for rho = 0 the line above turned it into 400p + acc - A
-                const uint32_t r = ((uint32_t)P * 800u - acc) % (uint32_t)P;
-                if (P * s3 + rho3 <= n2) out[-rho3] = (uint8_t)r;
+                // acc < 35 p (p-1) + p < 2^32 / p: the quotient by the magic multiply is exact
+                const uint32_t qq = __umulhi(acc[rho3], (uint32_t)(0xFFFFFFFFu / P + 1));
+                uint8_t* o = (rho3 <= room) ? out - rho3 : dummy;
+                *o = (uint8_t)(acc[rho3] - qq * (uint32_t)P);
             }
         }
         __syncthreads();
