@@ -20,8 +20,10 @@
 // and one output is  (A - sum_w dp4a(sEc[class][w], sHp[w][point])) mod p : one broadcast LDS.32 and
 // one DP4A per four multiply-adds.  The output is produced slab by slab (slab = all exponents with
 // a fixed I1 = p*s1 + rho1), staged in shared memory in the final guard-banded layout and written
-// to HBM with 16-byte coalesced stores.  Inside a slab the work items are (rho2, point (s2,s3)),
-// P*T(s1) of them, dealt to threads with rho2 (hence the class) uniform per warp.
+// to HBM with 16-byte coalesced stores.  KS consecutive slabs of one layer (they are contiguous in
+// HBM) form a phase; its work items are (slab, rho2, pair of points (s2,s3)), dealt to threads with
+// the class uniform per warp.  A thread handles two points at once so that every coefficient word
+// it loads feeds two DP4As (the kernel is bound by shared-memory load issue otherwise).
 //
 // Output layout: "lex43g" (qfs_shape.cuh) -- entry (I1,I2,I3,I4) at gbase(I1,I2) + I4, every run
 // followed by G guard zeros, ZPAD leading zeros.  The slab staged in shared memory uses the same
@@ -43,7 +45,10 @@ struct DeltaCfg {
     static constexpr int TMAX = (S::d + 1) * (S::d + 2) / 2;  // points (s2,s3) of the layer s1 = 0
     static constexpr int TPAD = (TMAX + 31) & ~31;
     static constexpr int RBH = (S::dh + 1) * (S::dh + 1);     // row bases of basis(dh) (bounds-checked path)
-    static constexpr int SLAB = qc2(S::D + 2) + S::G * (S::D + 1) + 32;
+    static constexpr int KS = (P >= 11) ? 1 : (P >= 7 ? 3 : P);  // slabs (consecutive rho1 of one layer) per phase
+    static QFS_HD constexpr int slab_bytes(int I1) { return qc2(S::D - I1 + 2) + S::G * (S::D - I1 + 1); }
+    static QFS_HD constexpr int slabs_bytes(int n) { int t = 0; for (int k = 0; k < n; ++k) t += slab_bytes(k); return t; }
+    static constexpr int SLAB = slabs_bytes(KS) + 32;
     static constexpr int OFF_EC = 0;                                   // uint32 [NCLS][9]
     static constexpr int OFF_HP = OFF_EC + qround16(NCLS * NWORD * 4);  // uint32 [9][TPAD]
     static constexpr int OFF_A = OFF_HP + NWORD * TPAD * 4;
@@ -53,21 +58,27 @@ struct DeltaCfg {
     static constexpr int SMEM = OFF_SLAB + qround16(SLAB) + 16;  // + sink bytes
 };
 
-// acc[rho3] = sum over the first NW tap words of class (rho1,rho2,rho3), for rho3 = 0..P-1
+// acc[u][rho3] = sum over the first NW tap words of class (rho1,rho2,rho3) for the points 2jq+u, u = 0,1
+// (hpq points at word 0 of the even point; the odd point is the next 32-bit word).
 template <int P, int NW>
 __device__ __forceinline__ void delta_classes(const uint32_t* __restrict__ ec, const uint32_t* __restrict__ hpq,
-                                              uint32_t (&acc)[P])
+                                              uint32_t (&acc)[2][P])
 {
     using C = DeltaCfg<P>;
-    uint32_t hp[NW];
+    uint2 hp[NW];
 #pragma unroll
-    for (int w = 0; w < NW; ++w) hp[w] = hpq[w * C::TPAD];
+    for (int w = 0; w < NW; ++w) hp[w] = *reinterpret_cast<const uint2*>(hpq + w * C::TPAD);
 #pragma unroll
     for (int rho3 = 0; rho3 < P; ++rho3) {
-        uint32_t a = 0;
+        uint32_t a0 = 0, a1 = 0;
 #pragma unroll
-        for (int w = 0; w < NW; ++w) a = __dp4a(ec[rho3 * C::NWORD + w], hp[w], a);
-        acc[rho3] = a;
+        for (int w = 0; w < NW; ++w) {
+            const uint32_t cw = ec[rho3 * C::NWORD + w];
+            a0 = __dp4a(cw, hp[w].x, a0);
+            a1 = __dp4a(cw, hp[w].y, a1);
+        }
+        acc[0][rho3] = a0;
+        acc[1][rho3] = a1;
     }
 }
 
@@ -154,12 +165,11 @@ k_delta(const uint8_t* __restrict__ h_all, const uint8_t* __restrict__ A_all, co
 
     // ---- slabs ---------------------------------------------------------------------------------
 #pragma unroll 1
-    for (int I1 = 0; I1 <= S::D; ++I1) {
-        const int s1 = I1 / P, rho1 = I1 - s1 * P;
-        const int n = S::D - I1;
+    for (int s1 = 0; s1 <= S::d; ++s1) {
+        const int I1 = P * s1;  // first slab of the layer
         const int ns = S::d - s1;
         const int T = (ns + 1) * (ns + 2) / 2;
-        if (rho1 == 0) {
+        {
             // packed h neighbourhoods of the layer's points: sHp[w][q] byte b = h[s - t_j], j = 4w+b
             for (int q = tid; q < T; q += C::NT) {
                 const uint32_t e = sTri[q];
@@ -190,42 +200,59 @@ k_delta(const uint8_t* __restrict__ h_all, const uint8_t* __restrict__ A_all, co
             }
             __syncthreads();
         }
-        const int goff = S::gbase(I1, 0);
-        const int bytes = qc2(n + 2) + S::G * (n + 1);  // the slab's runs with their guards
-        uint8_t* slab = sSlab + (((size_t)(gd + goff)) & 15);
+        for (int rho1_0 = 0; rho1_0 < P; rho1_0 += C::KS) {
+        const int ks = min(C::KS, P - rho1_0);
+        const int I1_0 = I1 + rho1_0;
+        const int goff = S::gbase(I1_0, 0);
+        int bytes = 0;  // the phase's slabs with their guards
+        for (int k = 0; k < ks; ++k) bytes += C::slab_bytes(I1_0 + k);
+        uint8_t* slab0 = sSlab + (((size_t)(gd + goff)) & 15);
         uint8_t* dummy = sSlab + qround16(C::SLAB) + (tid & 15);  // sink for the stores of non-exponents
-        const float invT = 1.0f / (float)T;
-        for (int i = tid; i < P * T; i += C::NT) {
-            const int rho2 = (int)(((float)i + 0.5f) * invT);
-            const int q = i - rho2 * T;
-            const uint32_t e = sTri[q];
-            const int kk = e & 255, s2 = e >> 8, s3 = kk - s2;
-            const int I2 = P * s2 + rho2;
-            const int n2 = n - I2;
-            if (n2 < 0) continue;
-            uint8_t* out = slab + ((I2 * (2 * n + 3 - I2)) >> 1) + S::G * I2 + (n2 - P * s3);  // position of rho3 = 0
+        const int TP2 = (T + 1) >> 1;
+        const float invT = 1.0f / (float)TP2;
+        for (int i = tid; i < ks * P * TP2; i += C::NT) {
+            const int c = (int)(((float)i + 0.5f) * invT);  // = slab-in-phase * P + rho2
+            const int jq = i - c * TP2;
+            const int k = (c * ((65536 + P - 1) / P)) >> 16, rho2 = c - k * P;
+            const int rho1 = rho1_0 + k;
+            const int n = S::D - I1_0 - k;
+            uint8_t* slab = slab0;
+#pragma unroll
+            for (int kk = 0; kk < C::KS - 1; ++kk)
+                if (kk < k) slab += C::slab_bytes(I1_0 + kk);
             const uint32_t* ec = sEc + ((rho1 * P + rho2) * P) * C::NWORD;
-            const uint32_t* hpq = sHp + q;
+            const uint32_t* hpq = sHp + 2 * jq;
             const int rs12 = rho1 + rho2;
             // |rho| = rs12 + rho3 leaves room for |t| <= 4 - ceil(|rho|/p): a prefix of 9/5/3/1 tap words.  The
             // prefix length is taken from rs12 alone (uniform over rho3; the extra words hold zeros).
-            uint32_t acc[P];
+            uint32_t acc[2][P];
             if (rs12 > 2 * P) delta_classes<P, 1>(ec, hpq, acc);
             else if (rs12 > P) delta_classes<P, 3>(ec, hpq, acc);
             else delta_classes<P, 5>(ec, hpq, acc);
-            if (rs12 == 0) {  // class rho = 0: all 35 taps, plus the phi(A) term
-                uint32_t a = acc[0];
+            const int I2base = rho2;
 #pragma unroll
-                for (int w = 5; w < 9; ++w) a = __dp4a(ec[w], hpq[w * C::TPAD], a);
-                acc[0] = a + (uint32_t)sA[qrowbase(S::d, s1, s2) + s3];
-            }
-            const int room = n2 - P * s3;  // rho3 <= room are real exponents (I4 >= 0)
+            for (int u = 0; u < 2; ++u) {
+                const int q = min(2 * jq + u, T - 1);
+                const uint32_t e = sTri[q];
+                const int kd = e & 255, s2 = e >> 8, s3 = kd - s2;
+                const int I2 = P * s2 + I2base;
+                const int n2 = n - I2;
+                if (rs12 == 0) {  // class rho = 0: all 35 taps, plus the phi(A) term
+                    uint32_t a = acc[u][0];
 #pragma unroll
-            for (int rho3 = 0; rho3 < P; ++rho3) {
-                // acc < 35 p (p-1) + p < 2^32 / p: the quotient by the magic multiply is exact
-                const uint32_t qq = __umulhi(acc[rho3], (uint32_t)(0xFFFFFFFFu / P + 1));
-                uint8_t* o = (rho3 <= room) ? out - rho3 : dummy;
-                *o = (uint8_t)(acc[rho3] - qq * (uint32_t)P);
+                    for (int w = 5; w < 9; ++w) a = __dp4a(ec[w], hpq[w * C::TPAD + u], a);
+                    acc[u][0] = a + (uint32_t)sA[qrowbase(S::d, s1, s2) + s3];
+                }
+                // rho3 <= room are real exponents (I4 >= 0); the odd point of a last pair does not exist
+                const int room = (2 * jq + u < T) ? n2 - P * s3 : -1;
+                uint8_t* out = slab + ((I2 * (2 * n + 3 - I2)) >> 1) + S::G * I2 + (n2 - P * s3);  // position of rho3 = 0
+#pragma unroll
+                for (int rho3 = 0; rho3 < P; ++rho3) {
+                    // acc < 35 p (p-1) + p < 2^32 / p: the quotient by the magic multiply is exact
+                    const uint32_t qq = __umulhi(acc[u][rho3], (uint32_t)(0xFFFFFFFFu / P + 1));
+                    uint8_t* o = (rho3 <= room) ? out - rho3 : dummy;
+                    *o = (uint8_t)(acc[u][rho3] - qq * (uint32_t)P);
+                }
             }
         }
         __syncthreads();
@@ -233,15 +260,16 @@ k_delta(const uint8_t* __restrict__ h_all, const uint8_t* __restrict__ A_all, co
             uint8_t* dst = gd + goff;
             int head = (16 - (int)(((size_t)dst) & 15)) & 15;
             if (head > bytes) head = bytes;
-            if (tid < head) { dst[tid] = slab[tid]; slab[tid] = 0; }
+            if (tid < head) { dst[tid] = slab0[tid]; slab0[tid] = 0; }
             const int nvec = (bytes - head) >> 4;
-            uint4* s4 = reinterpret_cast<uint4*>(slab + head);
+            uint4* s4 = reinterpret_cast<uint4*>(slab0 + head);
             uint4* d4 = reinterpret_cast<uint4*>(dst + head);
             for (int i = tid; i < nvec; i += C::NT) { d4[i] = s4[i]; s4[i] = make_uint4(0, 0, 0, 0); }
             const int done = head + (nvec << 4);
-            if (tid < bytes - done) { dst[done + tid] = slab[done + tid]; slab[done + tid] = 0; }
+            if (tid < bytes - done) { dst[done + tid] = slab0[done + tid]; slab0[done + tid] = 0; }
         }
         __syncthreads();
+        }  // phases of the layer
     }
 }
 
