@@ -60,7 +60,7 @@ struct qfs_ctx {
     qfs_stats stats = {};
     // device state
     DevBuf flags;                                   // int err, int queue, int count (+ pad)
-    DevBuf colinfo, groups;                         // per-p index tables for the matrix builder
+    DevBuf colinfo, groups, runs;                   // per-p index tables for the matrix builder
     DevBuf unrank;                                  // per-p unrank tables for the power chain
     DevBuf coeffs, heights, iters, list;            // batch-sized
     DevBuf g, h, A, E, delta, M, v1;                // chunk-sized
@@ -153,10 +153,13 @@ int build_tables(qfs_ctx* ctx)
             for (int c3 = 0; c1 + c2 + c3 <= S::d; ++c3) col[c++] = (uint32_t)c1 | ((uint32_t)c2 << 8) | ((uint32_t)c3 << 16);
         }
     if (c != S::N || gidx != S::ngroups) return fail(ctx, QFS_EINVAL, "internal: basis enumeration mismatch");
+    const std::vector<uint16_t> runs_lex = grp;  // column runs (c1,c2) in lex order
     // longest row groups first: the builder's CTAs then finish together
     std::stable_sort(grp.begin(), grp.end(), [](uint16_t a, uint16_t b) { return (a & 255) + (a >> 8) < (b & 255) + (b >> 8); });
     CU(ctx->colinfo.reserve(col.size() * 4));
     CU(ctx->groups.reserve(grp.size() * 2));
+    CU(ctx->runs.reserve(grp.size() * 2));
+    CU(cudaMemcpy(ctx->runs.ptr, runs_lex.data(), runs_lex.size() * 2, cudaMemcpyHostToDevice));
     CU(cudaMemcpy(ctx->colinfo.ptr, col.data(), col.size() * 4, cudaMemcpyHostToDevice));
     CU(cudaMemcpy(ctx->groups.ptr, grp.data(), grp.size() * 2, cudaMemcpyHostToDevice));
     {
@@ -175,6 +178,8 @@ int build_tables(qfs_ctx* ctx)
     CU(cudaFuncSetAttribute(k_power_full<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, PowerCfg<P>::FULL_SMEM));
     CU(cudaFuncSetAttribute(k_delta<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, DeltaCfg<P>::SMEM));
     CU(cudaFuncSetAttribute(k_chain<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, ChainCfg<P>::SMEM));
+    CU(cudaFuncSetAttribute(k_matrix<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, MatrixCfg<P>::SMEM));
+    CU(cudaFuncSetAttribute(k_matrix<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, MatrixCfg<P>::SMEM));
     return QFS_OK;
 }
 
@@ -229,11 +234,13 @@ int launch_matrix(qfs_ctx* ctx, int count, const uint8_t* v0, uint8_t* v1)
     using C = MatrixCfg<P>;
     const dim3 grid((unsigned)S::ngroups, (unsigned)((count + C::SLICE - 1) / C::SLICE));
     if (v0)
-        k_matrix<P, true><<<grid, C::NT, 0, ctx->stream>>>(ctx->delta.as<uint8_t>(), ctx->colinfo.as<uint32_t>(),
-                                                          ctx->groups.as<uint16_t>(), ctx->M.as<uint8_t>(), v0, v1, count);
+        k_matrix<P, true><<<grid, C::NT, C::SMEM, ctx->stream>>>(ctx->delta.as<uint8_t>(), ctx->colinfo.as<uint32_t>(),
+                                                                ctx->groups.as<uint16_t>(), ctx->runs.as<uint16_t>(),
+                                                                ctx->M.as<uint8_t>(), v0, v1, count);
     else
-        k_matrix<P, false><<<grid, C::NT, 0, ctx->stream>>>(ctx->delta.as<uint8_t>(), ctx->colinfo.as<uint32_t>(),
-                                                           ctx->groups.as<uint16_t>(), ctx->M.as<uint8_t>(), nullptr, nullptr, count);
+        k_matrix<P, false><<<grid, C::NT, C::SMEM, ctx->stream>>>(ctx->delta.as<uint8_t>(), ctx->colinfo.as<uint32_t>(),
+                                                                 ctx->groups.as<uint16_t>(), ctx->runs.as<uint16_t>(),
+                                                                 ctx->M.as<uint8_t>(), nullptr, nullptr, count);
     ctx->stats.kernel_launches++;
     CU(cudaGetLastError());
     return QFS_OK;
@@ -564,7 +571,7 @@ void qfs_destroy(qfs_ctx* ctx)
 {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
-    DevBuf* bufs[] = {&ctx->flags, &ctx->colinfo, &ctx->groups, &ctx->unrank, &ctx->coeffs, &ctx->heights, &ctx->iters, &ctx->list,
+    DevBuf* bufs[] = {&ctx->flags, &ctx->colinfo, &ctx->groups, &ctx->runs, &ctx->unrank, &ctx->coeffs, &ctx->heights, &ctx->iters, &ctx->list,
                       &ctx->g, &ctx->h, &ctx->A, &ctx->E, &ctx->delta, &ctx->M, &ctx->v1, &ctx->tapA, &ctx->tapB};
     for (DevBuf* b : bufs) b->release();
     for (auto& e : ctx->ev) if (e) cudaEventDestroy(e);
