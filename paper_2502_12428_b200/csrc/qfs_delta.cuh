@@ -30,7 +30,20 @@
 // guard-banded layout (guards stay zero: the flush re-zeroes what it copied), so the guards and
 // the zero pad are (re)written with every surface and need no separate memset.
 #pragma once
+#include <cooperative_groups.h>
+
 #include "qfs_shape.cuh"
+
+// 4x4 byte transpose: in[s] holds bytes (x, x+1, x+2, x+3) of source s; out[j] = bytes (in[0].bj, in[1].bj, in[2].bj, in[3].bj)
+__device__ __forceinline__ void transpose4x4(const uint32_t (&in)[4], uint32_t (&out)[4])
+{
+    const uint32_t t0 = __byte_perm(in[0], in[1], 0x5140), t1 = __byte_perm(in[2], in[3], 0x5140);
+    const uint32_t t2 = __byte_perm(in[0], in[1], 0x7362), t3 = __byte_perm(in[2], in[3], 0x7362);
+    out[0] = __byte_perm(t0, t1, 0x5410);
+    out[1] = __byte_perm(t0, t1, 0x7632);
+    out[2] = __byte_perm(t2, t3, 0x5410);
+    out[3] = __byte_perm(t2, t3, 0x7632);
+}
 
 template <int P>
 struct DeltaCfg {
@@ -83,7 +96,7 @@ __device__ __forceinline__ void delta_classes(const uint32_t* __restrict__ ec, c
 }
 
 template <int P>
-__global__ void __launch_bounds__(DeltaCfg<P>::NT)
+__global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(DeltaCfg<P>::NT)
 k_delta(const uint8_t* __restrict__ h_all, const uint8_t* __restrict__ A_all, const uint8_t* __restrict__ E_all,
         uint8_t* __restrict__ delta_all, int count)
 {
@@ -96,28 +109,36 @@ k_delta(const uint8_t* __restrict__ h_all, const uint8_t* __restrict__ A_all, co
     uint8_t* sH = smem + C::OFF_H;
     uint8_t* sSlab = smem + C::OFF_SLAB;
 
-    const int slot = blockIdx.x;
-    if (slot >= count) return;
+    // One CTA per surface, four CTAs (one quad of surfaces) per cluster: the quad's Delta is written
+    // byte-interleaved (qfs_shape.cuh), each CTA collecting its share of the four slabs over DSMEM.
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    const unsigned crank = cluster.block_rank();
+    const int slot = blockIdx.x;        // grid = 4 * quads; slots >= count are padding (their Delta is zero)
+    const bool live = slot < count;
     const int tid = threadIdx.x;
     const uint8_t* gh = h_all + (size_t)slot * S::Nh_pad;
     const uint8_t* gE = E_all + (size_t)slot * S::NE_pad;
     const uint8_t* sA = C::A_IN_SMEM ? smem + C::OFF_A : A_all + (size_t)slot * S::pitch;
-    uint8_t* gd = delta_all + (size_t)slot * S::Lg_pad;
+    uint8_t* gq = delta_all + (size_t)(slot >> 2) * S::quad_stride;  // the quad's interleaved Delta
+    const uint8_t* peer[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) peer[r] = cluster.map_shared_rank(sSlab, r);
 
     // ---- per-surface setup -------------------------------------------------------------------
-    if (C::A_IN_SMEM) {
+    if (C::A_IN_SMEM && live) {
         const uint4* a4 = reinterpret_cast<const uint4*>(A_all + (size_t)slot * S::pitch);
         for (int i = tid; i < S::pitch / 16; i += C::NT) reinterpret_cast<uint4*>(smem + C::OFF_A)[i] = a4[i];
     }
     for (int i = tid; i < qround16(C::SLAB) / 16; i += C::NT) reinterpret_cast<uint4*>(sSlab)[i] = make_uint4(0, 0, 0, 0);
-    for (int i = tid; i < S::ZPAD / 16; i += C::NT) reinterpret_cast<uint4*>(gd)[i] = make_uint4(0, 0, 0, 0);
+    for (int i = crank * C::NT + tid; i < 4 * S::ZPAD / 16; i += 4 * C::NT) reinterpret_cast<uint4*>(gq)[i] = make_uint4(0, 0, 0, 0);
     for (int e = tid; e < (S::d + 1) * (S::d + 1); e += C::NT) {  // points of a layer by diagonals kk = s2+s3
         const int kk = e / (S::d + 1), s2 = e - kk * (S::d + 1);
         if (s2 <= kk) sTri[kk * (kk + 1) / 2 + s2] = (uint16_t)(kk | (s2 << 8));
     }
     if (C::USE_BOX) {
         for (int i = tid; i < qround16(C::BOX) / 16; i += C::NT) reinterpret_cast<uint4*>(sH)[i] = make_uint4(0, 0, 0, 0);
-    } else {
+    } else if (live) {
         for (int i = tid; i < S::Nh_pad / 16; i += C::NT)
             reinterpret_cast<uint4*>(sH)[i] = reinterpret_cast<const uint4*>(gh)[i];
         uint16_t* rbh = reinterpret_cast<uint16_t*>(sH + S::Nh_pad);
@@ -127,7 +148,7 @@ k_delta(const uint8_t* __restrict__ h_all, const uint8_t* __restrict__ A_all, co
         }
     }
     // class table: sEc[c][w] byte b = -E[rho + p*t_j] mod p, j = 4w+b, taps ordered by |t| then lex; 0 outside deg 4p
-    for (int e = tid; e < C::NCLS * C::NWORD; e += C::NT) {
+    for (int e = tid; e < (live ? C::NCLS * C::NWORD : 0); e += C::NT) {
         const int c = e / C::NWORD, w = e - c * C::NWORD;
         const int rho1 = c / (P * P), rho2 = (c / P) % P, rho3 = c % P;
         uint32_t word = 0;
@@ -151,7 +172,7 @@ k_delta(const uint8_t* __restrict__ h_all, const uint8_t* __restrict__ A_all, co
         sEc[e] = word;
     }
     __syncthreads();
-    if (C::USE_BOX) {
+    if (C::USE_BOX && live) {
         for (int e = tid; e < (S::dh + 1) * (S::dh + 1); e += C::NT) {
             const int u1 = e / (S::dh + 1), u2 = e - u1 * (S::dh + 1);
             const int len = S::dh - u1 - u2;
@@ -171,7 +192,7 @@ k_delta(const uint8_t* __restrict__ h_all, const uint8_t* __restrict__ A_all, co
         const int T = (ns + 1) * (ns + 2) / 2;
         {
             // packed h neighbourhoods of the layer's points: sHp[w][q] byte b = h[s - t_j], j = 4w+b
-            for (int q = tid; q < T; q += C::NT) {
+            for (int q = tid; q < (live ? T : 0); q += C::NT) {
                 const uint32_t e = sTri[q];
                 const int kk = e & 255, s2 = e >> 8, s3 = kk - s2;
                 uint32_t word = 0;
@@ -206,11 +227,11 @@ k_delta(const uint8_t* __restrict__ h_all, const uint8_t* __restrict__ A_all, co
         const int goff = S::gbase(I1_0, 0);
         int bytes = 0;  // the phase's slabs with their guards
         for (int k = 0; k < ks; ++k) bytes += C::slab_bytes(I1_0 + k);
-        uint8_t* slab0 = sSlab + (((size_t)(gd + goff)) & 15);
+        uint8_t* slab0 = sSlab + (goff & 15);  // sSlab[0] <-> Delta offset goff & ~15
         uint8_t* dummy = sSlab + qround16(C::SLAB) + (tid & 15);  // sink for the stores of non-exponents
         const int TP2 = (T + 1) >> 1;
         const float invT = 1.0f / (float)TP2;
-        for (int i = tid; i < ks * P * TP2; i += C::NT) {
+        for (int i = tid; i < (live ? ks * P * TP2 : 0); i += C::NT) {
             const int c = (int)(((float)i + 0.5f) * invT);  // = slab-in-phase * P + rho2
             const int jq = i - c * TP2;
             const int k = (c * ((65536 + P - 1) / P)) >> 16, rho2 = c - k * P;
@@ -255,34 +276,41 @@ k_delta(const uint8_t* __restrict__ h_all, const uint8_t* __restrict__ A_all, co
                 }
             }
         }
-        __syncthreads();
-        {   // flush: slab and destination share their alignment mod 16
-            uint8_t* dst = gd + goff;
-            int head = (16 - (int)(((size_t)dst) & 15)) & 15;
-            if (head > bytes) head = bytes;
-            if (tid < head) { dst[tid] = slab0[tid]; slab0[tid] = 0; }
-            const int nvec = (bytes - head) >> 4;
-            uint4* s4 = reinterpret_cast<uint4*>(slab0 + head);
-            uint4* d4 = reinterpret_cast<uint4*>(dst + head);
-            for (int i = tid; i < nvec; i += C::NT) { d4[i] = s4[i]; s4[i] = make_uint4(0, 0, 0, 0); }
-            const int done = head + (nvec << 4);
-            if (tid < bytes - done) { dst[done + tid] = slab0[done + tid]; slab0[done + tid] = 0; }
+        cluster.sync();  // the four slabs of the quad are complete
+        {   // flush: groups of four consecutive Delta offsets x..x+3, interleaved over the quad's four surfaces
+            // into one 16-byte store.  The range is widened to whole groups: the bytes it adds in front are
+            // guard zeros of the previous phase, the ones behind are rewritten by the next phase.
+            const int x_lo = goff & ~3, x_hi = (goff + bytes + 3) & ~3;
+            const int ng = (x_hi - x_lo) >> 2;
+            const int per = (ng + 3) >> 2;  // each CTA of the cluster stores a contiguous quarter
+            const int g_end = min(ng, (int)(crank + 1) * per);
+            const int sbase = x_lo - (goff & ~15);
+            for (int gi = crank * per + tid; gi < g_end; gi += C::NT) {
+                uint32_t in[4], out[4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) in[r] = *reinterpret_cast<const uint32_t*>(peer[r] + sbase + 4 * gi);
+                transpose4x4(in, out);
+                *reinterpret_cast<uint4*>(gq + 4 * (size_t)(x_lo + 4 * gi)) = make_uint4(out[0], out[1], out[2], out[3]);
+            }
         }
+        cluster.sync();  // everyone has read this CTA's slab: clear it for the next phase
+        for (int i = tid; i < (bytes + 15 + 15) >> 4; i += C::NT) reinterpret_cast<uint4*>(sSlab)[i] = make_uint4(0, 0, 0, 0);
         __syncthreads();
         }  // phases of the layer
     }
 }
 
-// lex43g <-> lex.  TO_G = true: dense lex input -> guard-banded lex43g output (which must be zero-filled
-// beforehand); TO_G = false: lex43g input -> dense lex output.  Used by the stage taps only.
+// lex43g (quad-interleaved) <-> lex.  TO_G = true: dense lex input [surface][L] -> interleaved lex43g output
+// (which must be zero-filled beforehand); TO_G = false: the reverse.  Used by the stage taps only.
 template <int P, bool TO_G>
-__global__ void k_delta_flip(const uint8_t* __restrict__ in, size_t in_stride, uint8_t* __restrict__ out,
-                             size_t out_stride)
+__global__ void k_delta_flip(const uint8_t* __restrict__ dense, uint8_t* __restrict__ inter)
 {
     using S = Shape<P>;
     const int I1 = blockIdx.x;
-    const uint8_t* src = in + (size_t)blockIdx.y * in_stride;
-    uint8_t* dst = out + (size_t)blockIdx.y * out_stride;
+    const int slot = blockIdx.y;
+    const uint8_t* src = dense + (size_t)slot * S::L;
+    uint8_t* dst = const_cast<uint8_t*>(dense) + (size_t)slot * S::L;
+    uint8_t* q = inter + (size_t)(slot >> 2) * S::quad_stride + (slot & 3);
     const int n = S::D - I1;
     const int base = qc3(S::D + 3) - qc3(n + 3);
     const int total = qc2(n + 2);
@@ -295,7 +323,7 @@ __global__ void k_delta_flip(const uint8_t* __restrict__ in, size_t in_stride, u
         }
         const int rb = (lo * (2 * n + 3 - lo)) >> 1;
         const int I4 = (n - lo) - (e - rb);
-        const int gi = S::gbase(I1, lo) + I4;
-        if (TO_G) dst[gi] = src[base + e]; else dst[base + e] = src[gi];
+        const size_t gi = 4 * (size_t)(S::gbase(I1, lo) + I4);
+        if (TO_G) q[gi] = src[base + e]; else dst[base + e] = q[gi];
     }
 }

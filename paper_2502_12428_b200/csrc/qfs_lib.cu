@@ -178,8 +178,6 @@ int build_tables(qfs_ctx* ctx)
     CU(cudaFuncSetAttribute(k_power_full<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, PowerCfg<P>::FULL_SMEM));
     CU(cudaFuncSetAttribute(k_delta<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, DeltaCfg<P>::SMEM));
     CU(cudaFuncSetAttribute(k_chain<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, ChainCfg<P>::SMEM));
-    CU(cudaFuncSetAttribute(k_matrix<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, MatrixCfg<P>::SMEM));
-    CU(cudaFuncSetAttribute(k_matrix<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, MatrixCfg<P>::SMEM));
     return QFS_OK;
 }
 
@@ -194,6 +192,7 @@ template <int P>
 int reserve_chunk(qfs_ctx* ctx, size_t cap)
 {
     using S = Shape<P>;
+    cap = (cap + 3) & ~(size_t)3;  // whole quads: the Witt carry and the matrix builder work on four surfaces at a time
     CU(ctx->g.reserve(cap * S::pitch));
     CU(ctx->A.reserve(cap * S::pitch));
     CU(ctx->h.reserve(cap * S::Nh_pad));
@@ -220,7 +219,7 @@ int launch_power_full(qfs_ctx* ctx, const uint8_t* d_coeffs, const uint32_t* d_l
 template <int P>
 int launch_delta(qfs_ctx* ctx, int count)
 {
-    k_delta<P><<<count, DeltaCfg<P>::NT, DeltaCfg<P>::SMEM, ctx->stream>>>(ctx->h.as<uint8_t>(), ctx->A.as<uint8_t>(),
+    k_delta<P><<<4 * ((count + 3) / 4), DeltaCfg<P>::NT, DeltaCfg<P>::SMEM, ctx->stream>>>(ctx->h.as<uint8_t>(), ctx->A.as<uint8_t>(),
                                                                           ctx->E.as<uint8_t>(), ctx->delta.as<uint8_t>(), count);
     ctx->stats.kernel_launches++;
     CU(cudaGetLastError());
@@ -232,15 +231,14 @@ int launch_matrix(qfs_ctx* ctx, int count, const uint8_t* v0, uint8_t* v1)
 {
     using S = Shape<P>;
     using C = MatrixCfg<P>;
-    const dim3 grid((unsigned)S::ngroups, (unsigned)((count + C::SLICE - 1) / C::SLICE));
+    const int nquads = (count + 3) / 4;
+    const dim3 grid((unsigned)S::ngroups, (unsigned)((nquads + C::SLICE - 1) / C::SLICE));
     if (v0)
-        k_matrix<P, true><<<grid, C::NT, C::SMEM, ctx->stream>>>(ctx->delta.as<uint8_t>(), ctx->colinfo.as<uint32_t>(),
-                                                                ctx->groups.as<uint16_t>(), ctx->runs.as<uint16_t>(),
-                                                                ctx->M.as<uint8_t>(), v0, v1, count);
+        k_matrix<P, true><<<grid, C::NT, 0, ctx->stream>>>(ctx->delta.as<uint8_t>(), ctx->colinfo.as<uint32_t>(),
+                                                          ctx->groups.as<uint16_t>(), ctx->M.as<uint8_t>(), v0, v1, count);
     else
-        k_matrix<P, false><<<grid, C::NT, C::SMEM, ctx->stream>>>(ctx->delta.as<uint8_t>(), ctx->colinfo.as<uint32_t>(),
-                                                                 ctx->groups.as<uint16_t>(), ctx->runs.as<uint16_t>(),
-                                                                 ctx->M.as<uint8_t>(), nullptr, nullptr, count);
+        k_matrix<P, false><<<grid, C::NT, 0, ctx->stream>>>(ctx->delta.as<uint8_t>(), ctx->colinfo.as<uint32_t>(),
+                                                           ctx->groups.as<uint16_t>(), ctx->M.as<uint8_t>(), nullptr, nullptr, count);
     ctx->stats.kernel_launches++;
     CU(cudaGetLastError());
     return QFS_OK;
@@ -454,14 +452,15 @@ int run_stage_delta(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, uint8_t* delt
         CU(ctx->A.reserve((size_t)cnt * S::pitch));
         CU(ctx->h.reserve((size_t)cnt * S::Nh_pad));
         CU(ctx->E.reserve((size_t)cnt * S::NE_pad));
-        CU(ctx->delta.reserve((size_t)cnt * S::Lg_pad));
+        const size_t cnt4 = ((size_t)cnt + 3) & ~(size_t)3;
+        CU(ctx->delta.reserve(cnt4 * S::Lg_pad));
         CU(ctx->tapB.reserve((size_t)cnt * S::L));
         CU(cudaMemcpyAsync(ctx->tapA.ptr, coeffs + done * 35, (size_t)cnt * 35, cudaMemcpyDefault, ctx->stream));
         int rc = launch_power_full<P>(ctx, ctx->tapA.as<uint8_t>(), nullptr, cnt, nullptr);
         if (rc) return rc;
         if ((rc = launch_delta<P>(ctx, cnt))) return rc;
         dim3 grid(S::D + 1, cnt);
-        k_delta_flip<P, false><<<grid, 256, 0, ctx->stream>>>(ctx->delta.as<uint8_t>(), S::Lg_pad, ctx->tapB.as<uint8_t>(), S::L);
+        k_delta_flip<P, false><<<grid, 256, 0, ctx->stream>>>(ctx->tapB.as<uint8_t>(), ctx->delta.as<uint8_t>());
         CU(cudaGetLastError());
         CU(cudaMemcpyAsync(delta + done * (size_t)S::L, ctx->tapB.ptr, (size_t)cnt * S::L, cudaMemcpyDefault, ctx->stream));
         CU(cudaStreamSynchronize(ctx->stream));
@@ -480,11 +479,12 @@ int run_stage_matrix(qfs_ctx* ctx, const uint8_t* delta, size_t B, uint8_t* M)
         int rc;
         CU(ctx->tapB.reserve((size_t)cnt * S::L));
         CU(cudaMemcpyAsync(ctx->tapB.ptr, delta + done * (size_t)S::L, (size_t)cnt * S::L, cudaMemcpyDefault, ctx->stream));
-        CU(ctx->delta.reserve((size_t)cnt * S::Lg_pad));
-        CU(cudaMemsetAsync(ctx->delta.ptr, 0, (size_t)cnt * S::Lg_pad, ctx->stream));
-        CU(ctx->M.reserve((size_t)cnt * S::N * S::pitch));
+        const size_t cnt4 = ((size_t)cnt + 3) & ~(size_t)3;
+        CU(ctx->delta.reserve(cnt4 * S::Lg_pad));
+        CU(cudaMemsetAsync(ctx->delta.ptr, 0, cnt4 * S::Lg_pad, ctx->stream));
+        CU(ctx->M.reserve(cnt4 * S::N * S::pitch));
         dim3 grid(S::D + 1, cnt);
-        k_delta_flip<P, true><<<grid, 256, 0, ctx->stream>>>(ctx->tapB.as<uint8_t>(), S::L, ctx->delta.as<uint8_t>(), S::Lg_pad);
+        k_delta_flip<P, true><<<grid, 256, 0, ctx->stream>>>(ctx->tapB.as<uint8_t>(), ctx->delta.as<uint8_t>());
         CU(cudaGetLastError());
         if ((rc = launch_matrix<P>(ctx, cnt, nullptr, nullptr))) return rc;
         if ((rc = from_padded(ctx, M + done * (size_t)S::N * S::N, ctx->M.ptr, (size_t)cnt * S::N, S::N, S::pitch))) return rc;

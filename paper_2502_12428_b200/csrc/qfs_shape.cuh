@@ -17,6 +17,7 @@
 // zeros, and columns that can never match read the leading zero pad: the matrix builder needs
 // no validity predicates at all (see qfs_matrix.cuh).
 #pragma once
+#include <stddef.h>
 #include <stdint.h>
 
 #if defined(__CUDACC__)
@@ -57,6 +58,10 @@ struct Shape {
     static constexpr int nruns = (D + 1) * (D + 2) / 2;
     static constexpr int Lg = ZPAD + L + G * nruns;
     static constexpr int Lg_pad = qround16(Lg);
+    // Four surfaces (a "quad": slots 4q..4q+3 of a chunk) share one byte-interleaved Delta array:
+    // byte x of slot s sits at (s>>2)*quad_stride + 4*x + (s&3), so one aligned 32-bit load fetches the
+    // same Delta entry of the four surfaces (qfs_matrix.cuh gathers that way).
+    static constexpr size_t quad_stride = 4 * (size_t)Lg_pad;
     static QFS_HD constexpr int runindex(int I1, int I2) { return I1 * (D + 1) - I1 * (I1 - 1) / 2 + I2; }
     static QFS_HD constexpr int gbase(int I1, int I2) { return ZPAD + qrowbase(D, I1, I2) + G * runindex(I1, I2); }
 };
