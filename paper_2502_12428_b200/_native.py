@@ -100,4 +100,6 @@ def raise_for(rc, message):
         raise InternalInvariantError(message)
     if rc == QFS_ENOMEM:
         raise MemoryError(message)
+    if "no CUDA device" in message or "sm_100a" in message:
+        raise EngineUnavailableError(message + " (this package has no CPU fallback)")
     raise QfsplitError(f"CUDA failure: {message}")

@@ -1,0 +1,122 @@
+"""GPU tests of the drop-in Python layer and of the pipeline's batching edge cases (all through the C ABI)."""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+ROWS = json.load(open(os.path.join(GOLDEN, "k3_fixture_vectors.json")))
+
+
+def test_height_matrix_drop_in():
+    """Fermat trio of the reference's acceptance suite (tests/test_acceptance.py:92-100) and API parity."""
+    import paper_2502_12428_b200 as q
+    fermat5 = q.SurfaceProblem(5, 4, q.parse_poly("x1^4+x2^4+x3^4+x4^4", 4, 5))
+    assert q.height_matrix(fermat5) == q.HeightResult(1, 10, 0)
+    dwork5 = q.SurfaceProblem(5, 4, q.parse_poly("x1^4+x2^4+x3^4+x4^4+x1*x2*x3*x4", 4, 5))
+    assert q.height_matrix(dwork5) == q.HeightResult(math.inf, 10, 9)
+    fermat3 = q.SurfaceProblem(3, 4, q.parse_poly("x1^4+x2^4+x3^4+x4^4", 4, 3))
+    assert q.height_matrix(fermat3) == q.HeightResult(math.inf, 10, 9)
+    assert q.height_matrix(q.SurfaceProblem(3, 4, fermat3.f, 4)) == q.HeightResult(math.inf, 4, 3)
+    assert q.height_matrix(q.SurfaceProblem(5, 4, dwork5.f, 1)) == q.HeightResult(math.inf, 1, 0)
+    with pytest.raises(q.DomainError):
+        q.height_matrix(fermat5, algorithm="bogus")
+    r = [x for x in ROWS if x["p"] == 7 and x["height"] == 6][0]
+    assert q.height_of_coeffs(7, r["coeffs"]) == q.HeightResult(6, 10, 5)
+
+
+def test_verify_fixtures_on_gpu():
+    import paper_2502_12428_b200 as q
+    verdicts = q.verify_fixtures(open(q.fixtures_path()).read(), primes=[5, 7])
+    assert len(verdicts) == 22 and all(v.ok for v in verdicts)
+    assert [v.got for v in verdicts[:11]] == list(range(1, 11)) + [math.inf]
+
+
+def test_f11_published_rows():
+    """The five F_11 rows of the published table (extended suite of the reference, tests/test_acceptance.py:84-89);
+    12341 x 12341 operator, 152 MB per surface."""
+    import paper_2502_12428_b200 as q
+    rows = [r for r in ROWS if r["p"] == 11]
+    hs, its = q.height_batch(11, np.array([r["coeffs"] for r in rows], dtype=np.uint8))
+    assert [int(h) for h in hs] == [r["height"] for r in rows]
+    assert [int(i) for i in its] == [r["height"] - 1 for r in rows]
+
+
+def test_run_search_on_gpu_matches_reference():
+    import paper_2502_12428_b200 as q
+    z = np.load(os.path.join(GOLDEN, "heights_p5_seed0_w0_10000.npz"))
+    hist, found = q.run_search(q.SearchConfig(p=5, sample_count=10000, rng_seed=0, parallelism=1))
+    want = np.bincount(z["heights"].astype(int), minlength=11)
+    assert hist.infinite == want[0] and all(hist.counts.get(h, 0) == want[h] for h in range(1, 11))
+    assert found[-1].height == int(z["heights"].max())
+    h2, _ = q.run_search(q.SearchConfig(p=5, sample_count=2001, rng_seed=3, parallelism=2))
+    a, b = q.sample_block(5, 1001, 3, 0), q.sample_block(5, 1000, 3, 1)
+    hs, _ = q.height_batch(5, np.concatenate([a, b]))
+    assert h2.counts == {int(h): int(c) for h, c in enumerate(np.bincount(hs)) if c and h}
+
+
+@pytest.mark.parametrize("p,B", [(5, 0), (5, 1), (5, 3), (5, 5), (7, 6), (3, 9)])
+def test_ragged_batches_and_chunking(p, B):
+    """Batch sizes that are not whole quads, the empty batch, and hard-surface chunks smaller than the batch."""
+    import oracle
+    from paper_2502_12428_b200.engine import Engine
+    rng = np.random.default_rng([11, p])
+    coeffs = rng.integers(0, p, size=(B, 35)).astype(np.uint8)
+    coeffs[(coeffs == 0).all(axis=1), 0] = 1
+    # make sure the hard path is exercised: append known height>=2 rows of the golden stream
+    z = np.load(os.path.join(GOLDEN, f"heights_p{p}_seed0_w0_{ {3: 3000, 5: 10000, 7: 2000}[p] }.npz"))
+    hard = z["coeffs"][np.nonzero(z["heights"] != 1)[0][:B]]
+    coeffs = np.concatenate([coeffs, hard]) if B else coeffs
+    want = oracle.heights_batch(coeffs, p, 10) if len(coeffs) else (np.empty(0, np.int8),) * 2
+    eng = Engine(p, 0)
+    try:
+        for chunk in (0, 1, 5):
+            eng.set_chunk(chunk)
+            hs, its = eng.heights(coeffs, 10)
+            assert np.array_equal(hs, want[0]) and np.array_equal(its, want[1]), f"chunk={chunk}"
+    finally:
+        eng.close()
+
+
+def test_device_buffers_and_errors():
+    import torch
+    import paper_2502_12428_b200 as q
+    from paper_2502_12428_b200.engine import get_engine
+    z = np.load(os.path.join(GOLDEN, "heights_p5_seed0_w0_10000.npz"))
+    dev = torch.from_numpy(z["coeffs"][:2000]).cuda()
+    hs, its = get_engine(5, 0).heights(dev, 10)
+    assert hs.is_cuda and np.array_equal(hs.cpu().numpy(), z["heights"][:2000]) and np.array_equal(its.cpu().numpy(), z["iters"][:2000])
+    bad = z["coeffs"][:8].copy()
+    bad[3, 7] = 5  # not a residue mod 5: caught on the device, reported as the reference's DomainError
+    with pytest.raises(q.DomainError):
+        get_engine(5, 0).heights(torch.from_numpy(bad).cuda(), 10)
+    zero = z["coeffs"][:8].copy()
+    zero[2] = 0
+    with pytest.raises(q.DomainError):
+        get_engine(5, 0).heights(torch.from_numpy(zero).cuda(), 10)
+
+
+def test_large_batch_properties():
+    """Full-size batch (BASELINE.json configs[1]) through size-independent properties: heights are invariant under
+    scaling f by a unit and under permuting the variables (tests/test_height.py in the reference), and the
+    height-1 fraction is 1 - 1/p within 5 sigma (tests/test_acceptance.py:210-219)."""
+    import paper_2502_12428_b200 as q
+    from paper_2502_12428_b200.quartic import EXPONENTS, INDEX_OF
+    p, B = 5, 100000
+    rng = np.random.default_rng(2024)
+    c = rng.integers(0, p, size=(B, 35)).astype(np.uint8)
+    c[(c == 0).all(axis=1), 0] = 1
+    hs, its = q.height_batch(p, c)
+    frac = float((hs == 1).mean())
+    assert abs(frac - (1 - 1 / p)) < 5 * math.sqrt((1 / p) * (1 - 1 / p) / B)
+    assert np.array_equal(its, np.where(hs > 0, hs - 1, 9))
+    hs2, _ = q.height_batch(p, (c.astype(np.int64) * 3 % p).astype(np.uint8))
+    assert np.array_equal(hs, hs2)
+    perm = (2, 0, 3, 1)
+    idx = np.array([INDEX_OF[tuple(e[perm[k]] for k in range(4))] for e in EXPONENTS])
+    hs3, _ = q.height_batch(p, np.ascontiguousarray(c[:, idx]))
+    assert np.array_equal(hs, hs3)
