@@ -73,6 +73,19 @@ def measured_peaks():
         return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
 
 
+def measured_traffic(p, kernel, hard, launches):
+    """dram__bytes_read.sum + dram__bytes_write.sum of `kernel` per launch, scaled from the committed
+    `ncu --set full` capture (profiles/traffic.json: bytes per hard surface measured on a 4000-hard-surface
+    launch) to this run's surfaces per launch; None if no capture is on file."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            t = json.load(fh)
+        per = t[f"p{p}"][kernel]["dram_bytes_per_hard_surface"]
+        return per * hard / launches
+    except Exception:
+        return None
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled every 200 ms while the timed region runs."""
 
@@ -133,8 +146,9 @@ def algorithmic_bytes(p, iters_hard):
     ksum = int(iters_hard.sum())
     return {
         "delta": hard * L,                          # Delta written once
-        "matrix": hard * (N * N + L),               # Delta gathered, M written once
-        "matvec": ksum * N * N + (ksum + hard) * N,  # M streamed once per operator application
+        "matrix": hard * (N * N + L),               # Delta gathered, M written once (first operator application fused: no extra bytes)
+        "matvec": (ksum - hard) * N * N + ksum * N,  # M streamed once per FURTHER operator application (k_chain)
+        # SURVEY.md 8d per-surface figure bytes(k) = N^2 + k N^2 + 2 L + (k+1) N, summed over the hard surfaces
         "total": hard * (N * N + 2 * L) + ksum * N * N + (ksum + hard) * N,
     }
 
@@ -291,7 +305,8 @@ def gpu_line(args, p, res, world, with_cpu):
         "height_histogram": {str(k): int(v) for k, v in enumerate(np.bincount(heights.astype(np.int64), minlength=2)) if v},
         "stage_ms_per_step": stage,
         "roofline": {"bound": "hbm", "kernel": name, "achieved": ach, "peak": peak, "unit": "GB/s",
-                     "frac": ach / peak, "traffic": None, "algorithmic_bytes_per_launch": kbytes / max(1, res["stats"]["chunks"]),
+                     "frac": ach / peak, "traffic": measured_traffic(p, name, hard, max(1, res["stats"]["chunks"])),
+                     "algorithmic_bytes_per_launch": kbytes / max(1, res["stats"]["chunks"]),
                      "launches_per_step": res["stats"]["chunks"], "ms_per_step": kms, "peak_source": peak_src,
                      "all_kernels": {k: {"ms": v[1], "GBps": (v[2] / (v[1] * 1e-3) / 1e9 if v[1] > 0 else 0.0)} for k, v in kernels.items()}},
         "roofline_pipeline": {"algorithmic_bytes_per_step": ab["total"], "achieved": ab["total"] / (ms_step * 1e-3) / 1e9,
