@@ -55,6 +55,7 @@ struct qfs_ctx {
     cudaEvent_t ev[EV_COUNT] = {};
     cudaEvent_t ev_total[2] = {};
     size_t workspace_limit = 0;
+    size_t auto_limit = 0;                          // default workspace budget, fixed at first use
     size_t chunk_override = 0;
     std::string error;
     qfs_stats stats = {};
@@ -335,10 +336,13 @@ int run_heights(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, int bound, int8_t
         // chunk capacity from the workspace budget
         size_t limit = ctx->workspace_limit;
         if (!limit) {
-            size_t fr = 0, tot = 0;
-            CU(cudaMemGetInfo(&fr, &tot));
-            size_t held = ctx->g.cap + ctx->A.cap + ctx->h.cap + ctx->E.cap + ctx->delta.cap + ctx->M.cap + ctx->v1.cap;
-            limit = (size_t)((double)(fr + held) * 0.4);
+            if (!ctx->auto_limit) {  // asked once per context: cudaMemGetInfo costs milliseconds on a busy heap
+                size_t fr = 0, tot = 0;
+                CU(cudaMemGetInfo(&fr, &tot));
+                size_t held = ctx->g.cap + ctx->A.cap + ctx->h.cap + ctx->E.cap + ctx->delta.cap + ctx->M.cap + ctx->v1.cap;
+                ctx->auto_limit = (size_t)((double)(fr + held) * 0.4);
+            }
+            limit = ctx->auto_limit;
         }
         size_t cap = ctx->chunk_override ? ctx->chunk_override : std::max<size_t>(1, limit / per_surface_bytes<P>());
         cap = std::min<size_t>(cap, (size_t)hard);
