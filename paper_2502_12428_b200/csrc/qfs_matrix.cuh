@@ -31,8 +31,8 @@
 // row (coalesced 128-byte stores per warp and matrix).
 //
 // Fused first step.  When FUSE, each thread keeps its words of v0 = g (of the four surfaces) in
-// registers, adds dp4a(M word, v0 word) per row into a [surface][row][lane] shared accumulator, and the
-// CTA finishes the dot products of its rows:  v1[row] = (M g)[row] mod p.  About 80% of the
+// registers, accumulates dp4a(M word, v0 word) per row; warp-wide sums (REDUX) go to a [surface][row]
+// shared accumulator and the CTA finishes the dot products of its rows:  v1[row] = (M g)[row] mod p.  About 80% of the
 // surfaces that reach this stage are decided by v1[cap] != 0 (height 2), so their M is never read back.
 #pragma once
 #include "qfs_delta.cuh"  // transpose4x4
@@ -54,7 +54,7 @@ struct MatrixCfg {
 // sp[j][k]: address of the interleaved source word of column 4*word_j + k for the block's first row.
 template <int P, bool FUSE, int U>
 __device__ __forceinline__ void matrix_row(const uint8_t* const (&sp)[MatrixCfg<P>::WPT][4], uint32_t* const (&dst)[4],
-                                           int lastw, const uint32_t (&vw)[MatrixCfg<P>::WPT][4], int* accp)
+                                           int lastw, const uint32_t (&vw)[MatrixCfg<P>::WPT][4], int* accp, int lane)
 {
     using S = Shape<P>;
     using C = MatrixCfg<P>;
@@ -73,9 +73,12 @@ __device__ __forceinline__ void matrix_row(const uint8_t* const (&sp)[MatrixCfg<
             if (FUSE) part[s] = __dp4a(out[s], vw[j][s], part[s]);
         }
     }
-    if (FUSE) {
+    if (FUSE) {  // warp-wide sums in hardware (REDUX), one shared atomic per warp, surface and row
 #pragma unroll
-        for (int s = 0; s < 4; ++s) atomicAdd(accp + s * (C::MAXROWS * 32) - U * 32, (int)part[s]);
+        for (int s = 0; s < 4; ++s) {
+            const int tot = (int)__reduce_add_sync(0xffffffffu, part[s]);
+            if (lane == 0) atomicAdd(accp + s * C::MAXROWS - U, tot);
+        }
     }
 }
 
@@ -91,13 +94,13 @@ k_matrix(const uint8_t* __restrict__ delta_all, const uint32_t* __restrict__ col
 {
     using S = Shape<P>;
     using C = MatrixCfg<P>;
-    __shared__ int s_acc[FUSE ? 4 * C::MAXROWS * 32 : 1];
+    __shared__ int s_acc[FUSE ? 4 * C::MAXROWS : 1];  // [surface][r3]
 
     const int grp = groups[blockIdx.x];
     const int r1 = grp & 255, r2 = grp >> 8;
     const int R = S::d - r1 - r2;
     const int row0 = qrowbase(S::d, r1, r2);
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x, lane = tid & 31;
     const int nquads = (count + 3) >> 2;
     const int q_begin = blockIdx.y * C::SLICE;
     const int q_end = min(nquads, q_begin + C::SLICE);
@@ -124,13 +127,13 @@ k_matrix(const uint8_t* __restrict__ delta_all, const uint32_t* __restrict__ col
     }
     const int lastw = wj[C::WPT - 1] - tid;
     if (FUSE) {
-        for (int i = tid; i < 4 * C::MAXROWS * 32; i += C::NT) s_acc[i] = 0;
+        if (tid < 4 * C::MAXROWS) s_acc[tid] = 0;
         __syncthreads();
     }
     // Rows are walked from r3 = R down to 0 (t = R - r3 = 0..R), UNROLL at a time, so that the source
     // offset 4*p*t, the destination offset -t*pitch and the accumulator offset are immediates.
     const int nblk = (R + 1) / C::UNROLL, nrem = (R + 1) - nblk * C::UNROLL;
-    int* const accR = &s_acc[FUSE ? R * 32 + lane : 0];
+    int* const accR = &s_acc[FUSE ? R : 0];
 
     for (int quad = q_begin; quad < q_end; ++quad) {
         uint32_t* dst[4];
@@ -146,11 +149,11 @@ k_matrix(const uint8_t* __restrict__ delta_all, const uint32_t* __restrict__ col
         int* accp = accR;
 #pragma unroll 1
         for (int b = 0; b < nblk; ++b) {
-            matrix_row<P, FUSE, 0>(sp, dst, lastw, vw, accp);
-            matrix_row<P, FUSE, 1>(sp, dst, lastw, vw, accp);
+            matrix_row<P, FUSE, 0>(sp, dst, lastw, vw, accp, lane);
+            matrix_row<P, FUSE, 1>(sp, dst, lastw, vw, accp, lane);
             if (C::UNROLL == 4) {
-                matrix_row<P, FUSE, 2>(sp, dst, lastw, vw, accp);
-                matrix_row<P, FUSE, 3>(sp, dst, lastw, vw, accp);
+                matrix_row<P, FUSE, 2>(sp, dst, lastw, vw, accp, lane);
+                matrix_row<P, FUSE, 3>(sp, dst, lastw, vw, accp, lane);
             }
 #pragma unroll
             for (int j = 0; j < C::WPT; ++j)
@@ -158,33 +161,25 @@ k_matrix(const uint8_t* __restrict__ delta_all, const uint32_t* __restrict__ col
                 for (int k = 0; k < 4; ++k) sp[j][k] += C::UNROLL * 4 * P;
 #pragma unroll
             for (int s = 0; s < 4; ++s) dst[s] -= C::UNROLL * (S::pitch / 4);
-            accp -= C::UNROLL * 32;
+            accp -= C::UNROLL;
         }
-#pragma unroll 1
-        for (int b = 0; b < nrem; ++b) {
-            matrix_row<P, FUSE, 0>(sp, dst, lastw, vw, accp);
-#pragma unroll
-            for (int j = 0; j < C::WPT; ++j)
-#pragma unroll
-                for (int k = 0; k < 4; ++k) sp[j][k] += 4 * P;
-#pragma unroll
-            for (int s = 0; s < 4; ++s) dst[s] -= S::pitch / 4;
-            accp -= 32;
+        if (nrem > 0) matrix_row<P, FUSE, 0>(sp, dst, lastw, vw, accp, lane);
+        if (C::UNROLL == 4) {
+            if (nrem > 1) matrix_row<P, FUSE, 1>(sp, dst, lastw, vw, accp, lane);
+            if (nrem > 2) matrix_row<P, FUSE, 2>(sp, dst, lastw, vw, accp, lane);
         }
         // next quad of the slice: undo the row walk, step one quad stride
 #pragma unroll
         for (int j = 0; j < C::WPT; ++j)
 #pragma unroll
-            for (int k = 0; k < 4; ++k) sp[j][k] += S::quad_stride - 4 * P * (R + 1);
+            for (int k = 0; k < 4; ++k) sp[j][k] += S::quad_stride - 4 * P * C::UNROLL * nblk;
         if (FUSE) {
             __syncthreads();
-            for (int e = warp; e < 4 * (R + 1); e += C::NT / 32) {
-                const int s = e / (R + 1), r3 = e - s * (R + 1);
-                uint32_t a = (uint32_t)s_acc[(s * C::MAXROWS + r3) * 32 + lane];
-                s_acc[(s * C::MAXROWS + r3) * 32 + lane] = 0;
-#pragma unroll
-                for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-                if (lane == 0) v1_all[(4 * (size_t)quad + s) * S::pitch + row0 + r3] = (uint8_t)(a % (uint32_t)P);
+            if (tid < 4 * (R + 1)) {
+                const int s = tid / (R + 1), r3 = tid - s * (R + 1);
+                const uint32_t a = (uint32_t)s_acc[s * C::MAXROWS + r3];
+                s_acc[s * C::MAXROWS + r3] = 0;
+                v1_all[(4 * (size_t)quad + s) * S::pitch + row0 + r3] = (uint8_t)(a % (uint32_t)P);
             }
             __syncthreads();
         }
