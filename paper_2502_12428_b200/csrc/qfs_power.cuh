@@ -57,8 +57,14 @@ struct PowerCfg {
     static QFS_HD constexpr int rb_offset(int d) { return qrb_offset(d); }
     static constexpr int FED_RB = rb_offset(4 * J0 + 4);       // tables for degrees 4..4*J0
     static constexpr int FULL_RB = rb_offset(4 * P);           // tables for degrees 4..4(p-1)
-    static constexpr int FED_SMEM = FED_WARPS * 2 * FED_BUF + 2 * FED_RB;
-    static constexpr int FULL_SMEM = 2 * FULL_BUF + 2 * FULL_RB;
+    // cubes of the box-form products: side = largest OUTPUT coordinate (4*J0 resp. 4p) + 4 pad + 1, so that every
+    // read in[o - e_t] stays inside the cube (inputs of lower degree leave the rest zero)
+    static constexpr int FED_SB = 4 * J0 + 5;
+    static constexpr int FED_BOX = (J0 > 1) ? qround16(FED_SB * FED_SB * FED_SB) : 0;
+    static constexpr int FULL_SB = 4 * P + 5;
+    static constexpr int FULL_BOX = qround16(FULL_SB * FULL_SB * FULL_SB);
+    static constexpr int FED_SMEM = FED_WARPS * (2 * FED_BUF + FED_BOX) + 2 * FED_RB;
+    static constexpr int FULL_SMEM = FULL_BUF + FULL_BOX;
 };
 
 // term list of one quartic: packed j1 | j2<<4 | j3<<8 | j4<<12 | coef<<16, nonzero terms only
@@ -100,6 +106,48 @@ __device__ __forceinline__ void mul_by_f_full(const uint8_t* __restrict__ in, ui
     }
 }
 
+// Box form of the same product, used for the full levels.  The input lives in a zero-initialised cube
+// box[(a1+4)*SB^2 + (a2+4)*SB + (a3+4)] (4 zeros below every axis, zeros outside the simplex), so that
+// in[o - e_t] is one byte load at a COMPILE-TIME offset from the output's own cube index and needs no
+// bounds check; the 35 coefficients of f sit in registers (zero where f has no term).  Two instructions
+// per multiply-add instead of ~14.  out (lex order) = in * f mod MOD for outputs idx0, idx0+stride, ...
+template <int MOD, int SB>
+__device__ __forceinline__ void mul_by_f_box(const uint8_t* __restrict__ box, uint8_t* __restrict__ out, int dout,
+                                             const uint32_t* __restrict__ unrank_out, const uint32_t (&c)[35],
+                                             int idx0, int stride)
+{
+    const int nout = qc3(dout + 3);
+    for (int o = idx0; o < nout; o += stride) {
+        const uint32_t m = unrank_out[o];
+        const uint8_t* b = box + (((int)(m & 255) + 4) * SB + (int)((m >> 8) & 255) + 4) * SB + (int)(m >> 16) + 4;
+        uint32_t acc = 0;
+        int t = 0;
+#pragma unroll
+        for (int j1 = 0; j1 <= 4; ++j1)
+#pragma unroll
+            for (int j2 = 0; j2 <= 4 - j1; ++j2)
+#pragma unroll
+                for (int j3 = 0; j3 <= 4 - j1 - j2; ++j3) {
+                    acc += c[t] * b[-((j1 * SB + j2) * SB + j3)];
+                    ++t;
+                }
+        // acc <= 35 (MOD-1)^2 < 2^32 / MOD: the magic-multiply quotient is exact
+        out[o] = (uint8_t)(acc - __umulhi(acc, (uint32_t)(0xFFFFFFFFu / MOD + 1)) * (uint32_t)MOD);
+    }
+}
+
+// lex -> box copy of a degree-deg form (the cube's zeros outside the simplex are never touched)
+template <int SB>
+__device__ __forceinline__ void lex_to_box(const uint8_t* __restrict__ lex, uint8_t* __restrict__ box, int deg,
+                                           const uint32_t* __restrict__ unrank_deg, int idx0, int stride)
+{
+    const int n = qc3(deg + 3);
+    for (int o = idx0; o < n; o += stride) {
+        const uint32_t m = unrank_deg[o];
+        box[(((int)(m & 255) + 4) * SB + (int)((m >> 8) & 255) + 4) * SB + (int)(m >> 16) + 4] = lex[o];
+    }
+}
+
 // ---------------------------------------------------------------------------------------------
 template <int P>
 __global__ void __launch_bounds__(PowerCfg<P>::FED_WARPS * 32)
@@ -108,7 +156,7 @@ k_fedder(const uint8_t* __restrict__ coeffs, int count, const uint32_t* __restri
 {
     using C = PowerCfg<P>;
     extern __shared__ __align__(16) uint8_t smem[];
-    uint16_t* rb = reinterpret_cast<uint16_t*>(smem + C::FED_WARPS * 2 * C::FED_BUF);
+    uint16_t* rb = reinterpret_cast<uint16_t*>(smem + C::FED_WARPS * (2 * C::FED_BUF + C::FED_BOX));
     __shared__ uint32_t s_terms[C::FED_WARPS][36];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     fill_rb_tables<P>(rb, 4 * C::J0, tid, C::FED_WARPS * 32);
@@ -117,9 +165,12 @@ k_fedder(const uint8_t* __restrict__ coeffs, int count, const uint32_t* __restri
     const int sid = blockIdx.x * C::FED_WARPS + warp;
     if (sid >= count) return;
     const uint8_t* cf = coeffs + (size_t)35 * sid;
-    uint8_t* bufA = smem + (size_t)warp * 2 * C::FED_BUF;
+    uint8_t* bufA = smem + (size_t)warp * (2 * C::FED_BUF + C::FED_BOX);
     uint8_t* bufB = bufA + C::FED_BUF;
+    uint8_t* box = bufB + C::FED_BUF;  // cube of the box-form products (full levels)
     uint32_t* terms = s_terms[warp];
+    if (C::J0 > 1)
+        for (int i = lane; i < C::FED_BOX / 16; i += 32) reinterpret_cast<uint4*>(box)[i] = make_uint4(0, 0, 0, 0);
 
     // nonzero terms of f via warp ballot; lanes 0..31 hold coefficients 0..31, lanes 0..2 also 32..34
     const uint32_t* unrank4 = unrank + qunrank_offset(1);
@@ -151,12 +202,19 @@ k_fedder(const uint8_t* __restrict__ coeffs, int count, const uint32_t* __restri
 
     uint8_t* cur = bufA;
     uint8_t* nxt = bufB;
-    // full levels f^2 .. f^J0
+    // full levels f^2 .. f^J0 in box form (coefficients of f in registers, zero where f has no term)
+    if (C::J0 > 1) {
+        uint32_t c[35];
+#pragma unroll
+        for (int t = 0; t < 35; ++t) c[t] = cur[t];
 #pragma unroll 1
-    for (int j = 2; j <= C::J0; ++j) {
-        mul_by_f_full<P>(cur, nxt, 4 * (j - 1), rb + C::rb_offset(4 * (j - 1)), unrank + qunrank_offset(j), terms, nf, lane, 32);
-        __syncwarp();
-        uint8_t* t = cur; cur = nxt; nxt = t;
+        for (int j = 2; j <= C::J0; ++j) {
+            lex_to_box<C::FED_SB>(cur, box, 4 * (j - 1), unrank + qunrank_offset(j - 1), lane, 32);
+            __syncwarp();
+            mul_by_f_box<P, C::FED_SB>(box, nxt, 4 * j, unrank + qunrank_offset(j), c, lane, 32);
+            __syncwarp();
+            uint8_t* t = cur; cur = nxt; nxt = t;
+        }
     }
     // transition level j = J0+1:  R_j[K] = sum_J f[J] * F_J0[cap - K - J],  K in basis(dk), dk = 4(p-2-J0)
     {
@@ -218,12 +276,9 @@ k_power_full(const uint8_t* __restrict__ coeffs, const uint32_t* __restrict__ li
     constexpr int PSQ = P * P;
     constexpr int NT = C::FULL_NT;
     extern __shared__ __align__(16) uint8_t smem[];
-    uint8_t* bufA = smem;
-    uint8_t* bufB = smem + C::FULL_BUF;
-    uint16_t* rb = reinterpret_cast<uint16_t*>(smem + 2 * C::FULL_BUF);
-    __shared__ uint32_t s_terms[36];
+    uint8_t* cur = smem;                    // the current level, lex order
+    uint8_t* box = smem + C::FULL_BUF;      // the same level as a zero-padded cube (input of the next product)
     __shared__ uint8_t s_tau35[36];
-    __shared__ int s_nf;
 
     const int slot = blockIdx.x;
     if (slot >= count) return;
@@ -232,8 +287,8 @@ k_power_full(const uint8_t* __restrict__ coeffs, const uint32_t* __restrict__ li
     const int tid = threadIdx.x;
     const uint32_t* unrank4 = unrank + qunrank_offset(1);
 
-    fill_rb_tables<P>(rb, 4 * (P - 1), tid, NT);
-    if (tid < 32) {  // warp 0: Teichmuller lift and compacted term list
+    for (int i = tid; i < C::FULL_BOX / 16; i += NT) reinterpret_cast<uint4*>(box)[i] = make_uint4(0, 0, 0, 0);
+    if (tid < 32) {  // warp 0: Teichmuller lift tau(c) = c^p mod p^2 of the 35 coefficients
         const int lane = tid;
         uint32_t c[2] = {cf[lane], lane < 3 ? (uint32_t)cf[32 + lane] : 0u};
         uint32_t tau[2];
@@ -242,33 +297,20 @@ k_power_full(const uint8_t* __restrict__ coeffs, const uint32_t* __restrict__ li
         for (int q = 0; q < 2; ++q) {
             if (c[q] >= (uint32_t)P) { bad = true; c[q] = 0; }
             uint32_t t = 1;
-            for (int i = 0; i < P; ++i) t = t * c[q] % PSQ;  // tau(c) = c^p mod p^2
+            for (int i = 0; i < P; ++i) t = t * c[q] % PSQ;
             tau[q] = t;
         }
         const unsigned badm = __ballot_sync(0xffffffffu, bad);
-        const unsigned m0 = __ballot_sync(0xffffffffu, c[0] != 0);
-        const unsigned m1 = __ballot_sync(0xffffffffu, c[1] != 0);
-        if (lane == 0 && (badm || !(m0 | m1))) atomicOr(err, QFS_ERRBIT_INPUT);
+        const unsigned nz = __ballot_sync(0xffffffffu, (c[0] | c[1]) != 0);
+        if (lane == 0 && (badm || !nz)) atomicOr(err, QFS_ERRBIT_INPUT);
         s_tau35[lane] = (uint8_t)tau[0];
-        bufA[lane] = (uint8_t)tau[0];
-        if (lane < 3) { s_tau35[32 + lane] = (uint8_t)tau[1]; bufA[32 + lane] = (uint8_t)tau[1]; }
-        const int n0 = __popc(m0);
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-            const unsigned mq = q ? m1 : m0;
-            if ((q == 0 || lane < 3) && (mq >> lane & 1)) {
-                const uint32_t mm = unrank4[32 * q + lane];
-                const uint32_t j1 = mm & 255, j2 = (mm >> 8) & 255, j3 = mm >> 16;
-                s_terms[(q ? n0 : 0) + __popc(mq & ((1u << lane) - 1))] =
-                    j1 | (j2 << 4) | (j3 << 8) | ((4 - j1 - j2 - j3) << 12) | (tau[q] << 16);
-            }
-        }
-        if (lane == 0) s_nf = n0 + __popc(m1);
+        cur[lane] = (uint8_t)tau[0];
+        if (lane < 3) { s_tau35[32 + lane] = (uint8_t)tau[1]; cur[32 + lane] = (uint8_t)tau[1]; }
     }
     __syncthreads();
-    const int nf = s_nf;
-    uint8_t* cur = bufA;
-    uint8_t* nxt = bufB;
+    uint32_t c[35];  // f_T in registers: the multiplier of every level
+#pragma unroll
+    for (int t = 0; t < 35; ++t) c[t] = s_tau35[t];
     const size_t oN = (size_t)slot * S::pitch;
 
     if (P == 3) {  // H = f_T itself
@@ -276,9 +318,10 @@ k_power_full(const uint8_t* __restrict__ coeffs, const uint32_t* __restrict__ li
     }
 #pragma unroll 1
     for (int k = 2; k <= P; ++k) {
-        mul_by_f_full<PSQ>(cur, nxt, 4 * (k - 1), rb + C::rb_offset(4 * (k - 1)), unrank + qunrank_offset(k), s_terms, nf, tid, NT);
+        lex_to_box<C::FULL_SB>(cur, box, 4 * (k - 1), unrank + qunrank_offset(k - 1), tid, NT);
         __syncthreads();
-        { uint8_t* t = cur; cur = nxt; nxt = t; }
+        mul_by_f_box<PSQ, C::FULL_SB>(box, cur, 4 * k, unrank + qunrank_offset(k), c, tid, NT);
+        __syncthreads();
         if (k == P - 2) {
             for (int i = tid; i < S::Nh; i += NT) h_out[(size_t)slot * S::Nh_pad + i] = (uint8_t)(cur[i] % P);
         } else if (k == P - 1) {
@@ -303,8 +346,8 @@ k_power_full(const uint8_t* __restrict__ coeffs, const uint32_t* __restrict__ li
             if (tid < 35) {  // subtract tau(a_J) at exponent p*J
                 const uint32_t mm = unrank4[tid];
                 const int idx = qrowbase(S::dE, P * (mm & 255), P * ((mm >> 8) & 255)) + P * (mm >> 16);
-                const uint32_t c = cf[tid] < P ? cf[tid] : 0;
-                cur[idx] = (uint8_t)((cur[idx] + PSQ - (c ? s_tau35[tid] : 0)) % PSQ);
+                const uint32_t cc = cf[tid] < P ? cf[tid] : 0;
+                cur[idx] = (uint8_t)((cur[idx] + PSQ - (cc ? s_tau35[tid] : 0)) % PSQ);
             }
             __syncthreads();
             int bad = 0;
