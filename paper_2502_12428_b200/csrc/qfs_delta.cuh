@@ -48,7 +48,7 @@ __device__ __forceinline__ void transpose4x4(const uint32_t (&in)[4], uint32_t (
 template <int P>
 struct DeltaCfg {
     using S = Shape<P>;
-    static constexpr int NT = (P >= 11) ? 512 : (P >= 7 ? 256 : (P >= 5 ? 128 : 64));
+    static constexpr int NT = (P >= 11) ? 512 : (P >= 7 ? 512 : (P >= 5 ? 256 : 64));
     static constexpr bool USE_BOX = (P < 11);  // p = 11: no room for the box; h is read with bounds checks
     static constexpr bool A_IN_SMEM = (P < 11);
     static constexpr int SB = S::dh + 9;       // box side: 4 zeros below, 4 above
