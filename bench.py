@@ -36,15 +36,8 @@ SHAPES = {3: (165, 2925), 5: (969, 91881), 7: (2925, 818805), 11: (12341, 143917
 
 def sample_block(p, count, seed, worker):
     """`count` coefficient vectors exactly as search._worker_block draws them (search.py:103,92-98)."""
-    rng = np.random.default_rng([seed, worker])
-    out = np.empty((count, 35), dtype=np.uint8)
-    for i in range(count):
-        while True:
-            v = rng.integers(0, p, size=35)
-            if v.any():
-                break
-        out[i] = v
-    return out
+    from paper_2502_12428_b200.search import sample_block as sb
+    return sb(p, count, seed, worker)
 
 
 def cached_block(p, count, seed, worker):

@@ -126,13 +126,28 @@ def sample_surface(rng, p: int, n: int = 4) -> Quartic:
     return Quartic(sample_coeffs(rng, p), p)
 
 
+def sample_rows(rng, p: int, count: int) -> np.ndarray:
+    """The next `count` samples of search.sample_surface drawn from `rng`, vectorised.
+
+    `rng.integers(0, p, size=(m, 35))` consumes the bit stream exactly like m successive
+    `rng.integers(0, p, size=35)` calls (numpy draws bounded int64 values one by one with no state carried
+    between calls; pinned against the reference's own seeded dumps in tests/test_host_api.py), and the
+    reference keeps the first nonzero draw of every attempt loop -- i.e. the samples are the draws with the
+    all-zero rows (probability p^-35) removed.
+    """
+    out = np.empty((count, NCOEFF), dtype=np.uint8)
+    have = 0
+    while have < count:
+        draws = rng.integers(0, p, size=(count - have, NCOEFF))
+        keep = draws[draws.any(axis=1)]
+        out[have:have + len(keep)] = keep
+        have += len(keep)
+    return out
+
+
 def sample_block(p: int, count: int, seed: int, worker: int) -> np.ndarray:
     """The `count` coefficient vectors worker `worker` draws in search._worker_block (search.py:103,108)."""
-    rng = np.random.default_rng([seed, worker])
-    out = np.empty((count, NCOEFF), dtype=np.uint8)
-    for i in range(count):
-        out[i] = sample_coeffs(rng, p)
-    return out
+    return sample_rows(np.random.default_rng([seed, worker]), p, count)
 
 
 # ---- run_search -------------------------------------------------------------------------------------------
@@ -225,50 +240,100 @@ def run_search(cfg: SearchConfig, devices=None, compute=None):
 # ---- spectrum search (paper section 7) --------------------------------------------------------
 
 def spectrum_search(p: int, block: int = 100000, rng_seed: int = 0, bound: int = 10, max_blocks: int = 1000,
-                    devices=None, compute=None, want=None):
+                    devices=None, compute=None, want=None, progress=None):
     """Sample seeded blocks until every height in `want` (default 1..bound and infinity) has a witness.
 
-    Block b of device lane k uses the reference stream `default_rng([rng_seed, b])`, so any witness can be
-    regenerated from (rng_seed, b, index).  Returns (witnesses {height code: (block, index, Quartic)},
-    HeightHistogram, blocks_done); height code 0 = infinity.
+    Block b uses the reference stream `default_rng([rng_seed, b])`, so any witness can be regenerated from
+    (rng_seed, b, index).  Blocks are sampled on a host thread ahead of the GPUs (one consumer thread per
+    device) and retired in block order, so the result does not depend on the number of devices.
+    Returns (witnesses {height code: (block, index, Quartic)}, HeightHistogram, blocks_done); height code
+    0 = infinity.  `progress(blocks_done, hist, witnesses)` is called after every retired block.
     """
+    import queue
     devs = [0] if devices is None else [int(d) for d in devices]
     want = set(range(0, bound + 1)) if want is None else {0 if (isinstance(h, float) and math.isinf(h)) else int(h) for h in want}
     hist = HeightHistogram(bound)
     witnesses = {}
-    b = 0
-    while b < max_blocks and not want.issubset(witnesses):
-        wave = list(range(b, min(max_blocks, b + len(devs))))
-        out = [None] * len(wave)
-        errors = []
+    todo = queue.Queue(maxsize=2 * len(devs))
+    done = {}
+    cond = threading.Condition()
+    stop = threading.Event()
+    errors = []
 
-        def run(k, blk):
-            try:
-                coeffs = sample_block(p, block, rng_seed, blk)
+    def produce():
+        try:
+            for blk in range(max_blocks):
+                if stop.is_set():
+                    break
+                item = (blk, sample_block(p, block, rng_seed, blk))
+                while not stop.is_set():
+                    try:
+                        todo.put(item, timeout=0.05)
+                        break
+                    except queue.Full:
+                        pass
+        except Exception as exc:
+            errors.append(exc)
+        finally:
+            for _ in devs:
+                while True:
+                    try:
+                        todo.put(None, timeout=0.05)
+                        break
+                    except queue.Full:
+                        if stop.is_set():
+                            try:
+                                todo.get_nowait()
+                            except queue.Empty:
+                                pass
+
+    def consume(dev):
+        try:
+            while True:
+                item = todo.get()
+                if item is None:
+                    break
+                blk, coeffs = item
+                if stop.is_set():
+                    continue
                 if compute is None:
-                    codes, _ = height_batch(p, coeffs, bound, devices=[devs[k]])
+                    codes, _ = height_batch(p, coeffs, bound, devices=[dev])
                 else:
-                    codes, _ = compute(p, coeffs, bound, devs[k])
-                out[k] = (coeffs, np.asarray(codes))
-            except Exception as exc:
-                errors.append(exc)
+                    codes, _ = compute(p, coeffs, bound, dev)
+                with cond:
+                    done[blk] = (coeffs, np.asarray(codes))
+                    cond.notify_all()
+        except Exception as exc:
+            errors.append(exc)
+            with cond:
+                cond.notify_all()
 
-        threads = [threading.Thread(target=run, args=(k, blk)) for k, blk in enumerate(wave)]
-        for t in threads:
-            t.start()
-        for t in threads:
-            t.join()
-        if errors:
-            raise errors[0]
-        for blk, (coeffs, codes) in zip(wave, out):
-            hist.record_codes(codes)
-            for h in np.unique(codes):
-                h = int(h)
-                if h not in witnesses:
-                    i = int(np.nonzero(codes == h)[0][0])
-                    witnesses[h] = (blk, i, Quartic(coeffs[i], p))
-        b += len(wave)
-    return witnesses, hist, b
+    threads = [threading.Thread(target=produce, daemon=True)] + [threading.Thread(target=consume, args=(d,), daemon=True) for d in devs]
+    for t in threads:
+        t.start()
+    nxt = 0
+    while nxt < max_blocks and not want.issubset(witnesses) and not errors:
+        with cond:
+            while nxt not in done and not errors:
+                cond.wait(timeout=0.1)
+            if errors:
+                break
+            coeffs, codes = done.pop(nxt)
+        hist.record_codes(codes)
+        for h in np.unique(codes):
+            h = int(h)
+            if h not in witnesses:
+                i = int(np.nonzero(codes == h)[0][0])
+                witnesses[h] = (nxt, i, Quartic(coeffs[i], p))
+        nxt += 1
+        if progress is not None:
+            progress(nxt, hist, witnesses)
+    stop.set()
+    for t in threads:
+        t.join(timeout=60)
+    if errors:
+        raise errors[0]
+    return witnesses, hist, nxt
 
 
 def spectrum_rows(witnesses) -> str:
