@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -14,6 +15,7 @@
 #include "qfs_chain.cuh"
 #include "qfs_delta.cuh"
 #include "qfs_matrix.cuh"
+#include "qfs_matrix_staged.cuh"
 #include "qfs_power.cuh"
 #include "qfs_shape.cuh"
 
@@ -66,6 +68,11 @@ struct qfs_ctx {
     DevBuf coeffs, heights, iters, list;            // batch-sized
     DevBuf g, h, A, E, delta, M, v1;                // chunk-sized
     DevBuf tapA, tapB;                              // staging for the stage taps
+    DevBuf items, vacc;                             // staged matrix builder: panel work list, 32-bit v1 accumulators
+    int n_items = 0;
+    size_t staged_smem = 0;
+    int staged_bufwords = 0;
+    int matrix_version = 6;                         // 6 = shared-memory staged builder, 4 = direct gather (QFS_MATRIX_V)
     int* h_flags = nullptr;                         // pinned mirror of flags
 };
 
@@ -175,6 +182,63 @@ int build_tables(qfs_ctx* ctx)
         CU(ctx->unrank.reserve(un.size() * 4));
         CU(cudaMemcpy(ctx->unrank.ptr, un.data(), un.size() * 4, cudaMemcpyHostToDevice));
     }
+    {   // panels of the staged matrix builder (qfs_matrix_staged.cuh)
+        using SC = StagedCfg<P>;
+        std::vector<int> c1w(SC::WORDS);  // block c1 of the last valid column of each 32-bit word of a row
+        for (int w = 0; w < SC::WORDS; ++w) c1w[w] = (int)(col[std::min(4 * w + 3, S::N - 1)] & 255);
+        struct Tmp { PanelItem it; long work; int staged; };
+        std::vector<Tmp> tmp;
+        int max_staged = 0;
+        for (int r1 = 0; r1 <= S::d; ++r1)
+            for (int r2 = 0; r1 + r2 <= S::d; ++r2) {
+                auto piece = [&](int c1, int c2min) { int a4, b4; return staged_piece<P>(r1, r2, c1, c2min, a4, b4) ? b4 - a4 : 0; };
+                auto words_of = [&](int lo, int hi, int& wlo) {
+                    int n = 0; wlo = -1;
+                    for (int w = 0; w < SC::WORDS; ++w) if (c1w[w] >= lo && c1w[w] <= hi) { if (wlo < 0) wlo = w; ++n; }
+                    return n;
+                };
+                auto emit = [&](int lo, int hi) {
+                    int wlo, n = words_of(lo, hi, wlo);
+                    if (n == 0) return true;
+                    int staged = (lo > 0) ? piece(lo - 1, std::max(0, S::d - lo)) : 0;  // head: last two runs of block lo-1
+                    for (int c1 = lo; c1 <= hi; ++c1) staged += piece(c1, 0);
+                    if (n > SC::MAXW || staged > SC::BUDGET) return false;
+                    PanelItem it{(uint8_t)r1, (uint8_t)r2, (uint8_t)lo, (uint8_t)hi, (uint16_t)wlo, (uint16_t)n};
+                    tmp.push_back({it, (long)n * (S::d - r1 - r2 + 1), staged});
+                    max_staged = std::max(max_staged, staged);
+                    return true;
+                };
+                int lo = 0;
+                while (lo <= S::d) {
+                    // longest block range [lo, hi] that fits; never start a panel in the last two (tiny) blocks
+                    int hi = lo, dummy;
+                    auto fits = [&](int h) {
+                        int st = (lo > 0) ? piece(lo - 1, std::max(0, S::d - lo)) : 0;
+                        for (int c1 = lo; c1 <= h; ++c1) st += piece(c1, 0);
+                        return st <= SC::BUDGET && words_of(lo, h, dummy) <= SC::MAXW;
+                    };
+                    while (hi < S::d && fits(hi + 1)) ++hi;
+                    if (hi >= S::d - 2) {
+                        if (!fits(S::d)) { if (lo >= S::d - 2) return fail(ctx, QFS_EINVAL, "internal: panel tail does not fit"); hi = S::d - 3; }
+                        else hi = S::d;
+                    }
+                    if (hi < lo || !emit(lo, hi)) return fail(ctx, QFS_EINVAL, "internal: panel does not fit the shared-memory budget");
+                    lo = hi + 1;
+                }
+            }
+        std::stable_sort(tmp.begin(), tmp.end(), [](const Tmp& a, const Tmp& b) { return a.work > b.work; });
+        std::vector<PanelItem> items(tmp.size());
+        for (size_t i = 0; i < tmp.size(); ++i) items[i] = tmp[i].it;
+        if (!SC::MULTI && (int)items.size() != S::ngroups) return fail(ctx, QFS_EINVAL, "internal: expected one panel per row group");
+        ctx->n_items = (int)items.size();
+        ctx->staged_bufwords = SC::ZW + max_staged;
+        ctx->staged_smem = 2 * (size_t)ctx->staged_bufwords * 4;
+        CU(ctx->items.reserve(items.size() * sizeof(PanelItem)));
+        CU(cudaMemcpy(ctx->items.ptr, items.data(), items.size() * sizeof(PanelItem), cudaMemcpyHostToDevice));
+        CU(cudaFuncSetAttribute(k_matrix_staged<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->staged_smem));
+        CU(cudaFuncSetAttribute(k_matrix_staged<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->staged_smem));
+        if (const char* e = getenv("QFS_MATRIX_V")) ctx->matrix_version = atoi(e);
+    }
     CU(cudaFuncSetAttribute(k_fedder<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, PowerCfg<P>::FED_SMEM));
     CU(cudaFuncSetAttribute(k_power_full<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, PowerCfg<P>::FULL_SMEM));
     CU(cudaFuncSetAttribute(k_delta<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, DeltaCfg<P>::SMEM));
@@ -233,6 +297,34 @@ int launch_matrix(qfs_ctx* ctx, int count, const uint8_t* v0, uint8_t* v1)
     using S = Shape<P>;
     using C = MatrixCfg<P>;
     const int nquads = (count + 3) / 4;
+    if (ctx->matrix_version == 6) {
+        using SC = StagedCfg<P>;
+        const dim3 sgrid((unsigned)ctx->n_items, (unsigned)((nquads + SC::SLICE - 1) / SC::SLICE));
+        if (v0) {
+            const size_t nv = 4 * (size_t)nquads * S::pitch;
+            if (SC::MULTI) {
+                CU(ctx->vacc.reserve(nv * sizeof(int)));
+                CU(cudaMemsetAsync(ctx->vacc.ptr, 0, nv * sizeof(int), ctx->stream));
+            }
+            k_matrix_staged<P, true><<<sgrid, SC::NTL, ctx->staged_smem, ctx->stream>>>(
+                ctx->delta.as<uint8_t>(), ctx->colinfo.as<uint32_t>(), ctx->items.as<PanelItem>(), ctx->M.as<uint8_t>(), v0, v1,
+                ctx->vacc.as<int>(), count, ctx->staged_bufwords);
+            ctx->stats.kernel_launches++;
+            CU(cudaGetLastError());
+            if (SC::MULTI) {
+                k_vec_finish<P><<<(unsigned)((nv + 255) / 256), 256, 0, ctx->stream>>>(ctx->vacc.as<int>(), v1, nv);
+                ctx->stats.kernel_launches++;
+                CU(cudaGetLastError());
+            }
+        } else {
+            k_matrix_staged<P, false><<<sgrid, SC::NTL, ctx->staged_smem, ctx->stream>>>(
+                ctx->delta.as<uint8_t>(), ctx->colinfo.as<uint32_t>(), ctx->items.as<PanelItem>(), ctx->M.as<uint8_t>(), nullptr,
+                nullptr, nullptr, count, ctx->staged_bufwords);
+            ctx->stats.kernel_launches++;
+            CU(cudaGetLastError());
+        }
+        return QFS_OK;
+    }
     const dim3 grid((unsigned)S::ngroups, (unsigned)((nquads + C::SLICE - 1) / C::SLICE));
     if (v0)
         k_matrix<P, true><<<grid, C::NT, 0, ctx->stream>>>(ctx->delta.as<uint8_t>(), ctx->colinfo.as<uint32_t>(),
@@ -576,7 +668,7 @@ void qfs_destroy(qfs_ctx* ctx)
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     DevBuf* bufs[] = {&ctx->flags, &ctx->colinfo, &ctx->groups, &ctx->runs, &ctx->unrank, &ctx->coeffs, &ctx->heights, &ctx->iters, &ctx->list,
-                      &ctx->g, &ctx->h, &ctx->A, &ctx->E, &ctx->delta, &ctx->M, &ctx->v1, &ctx->tapA, &ctx->tapB};
+                      &ctx->g, &ctx->h, &ctx->A, &ctx->E, &ctx->delta, &ctx->M, &ctx->v1, &ctx->tapA, &ctx->tapB, &ctx->items, &ctx->vacc};
     for (DevBuf* b : bufs) b->release();
     for (auto& e : ctx->ev) if (e) cudaEventDestroy(e);
     for (auto& e : ctx->ev_total) if (e) cudaEventDestroy(e);
