@@ -132,6 +132,23 @@ int qfs_stage_matrix(qfs_ctx *ctx, const uint8_t *delta, size_t B, uint8_t *M);
 int qfs_stage_matvec_chain(qfs_ctx *ctx, const uint8_t *M, const uint8_t *v0, size_t B, int max_steps,
                            uint8_t *trace, int8_t *heights, int8_t *iters);
 
+/* ---- export ---------------------------------------------------------------
+ * Operator matrices of B quartics (given by their coefficient vectors) in the
+ * reference's export layout: M16[B][N][N] row-major uint16 little-endian --
+ * exactly the entry block of matrix_to_bytes (mtsmatrix.py:350-365) and the
+ * values matrix_to_text prints (mtsmatrix.py:301-306); the caller adds the
+ * "QFSMTX01" magic and the six-word header.  Replaces the body of cmd_matrix
+ * (cli.py:108-122): power_mod_p + delta1 + build_mts.  M16 may be host or
+ * device memory. */
+int qfs_export_matrix(qfs_ctx *ctx, const uint8_t *coeffs, size_t B, uint16_t *M16);
+
+/* ---- test hook -------------------------------------------------------------
+ * Overwrites every device workspace the context currently holds with `byte`.
+ * No kernel may depend on what a workspace held before the call that uses it
+ * (recycled device memory is not zero); tests/test_gpu_api.py poisons the
+ * workspaces between calls to prove it. */
+int qfs_debug_fill_workspaces(qfs_ctx *ctx, int byte);
+
 #ifdef __cplusplus
 }
 #endif

@@ -21,6 +21,7 @@ EXPORTS = (
     "qfs_version", "qfs_get_shape", "qfs_create", "qfs_destroy", "qfs_last_error",
     "qfs_set_workspace_limit", "qfs_set_chunk", "qfs_heights", "qfs_get_stats",
     "qfs_stage_power", "qfs_stage_delta", "qfs_stage_matrix", "qfs_stage_matvec_chain",
+    "qfs_export_matrix", "qfs_debug_fill_workspaces",
 )
 
 
@@ -86,6 +87,8 @@ def load():
     lib.qfs_stage_delta.argtypes = [vp, u8p, sz, u8p]
     lib.qfs_stage_matrix.argtypes = [vp, u8p, sz, u8p]
     lib.qfs_stage_matvec_chain.argtypes = [vp, u8p, u8p, sz, ctypes.c_int, u8p, i8p, i8p]
+    lib.qfs_export_matrix.argtypes = [vp, u8p, sz, vp]
+    lib.qfs_debug_fill_workspaces.argtypes = [vp, ctypes.c_int]
     _lib = lib
     return lib
 

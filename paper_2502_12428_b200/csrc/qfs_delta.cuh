@@ -225,8 +225,10 @@ k_delta(const uint8_t* __restrict__ h_all, const uint8_t* __restrict__ A_all, co
         const int ks = min(C::KS, P - rho1_0);
         const int I1_0 = I1 + rho1_0;
         const int goff = S::gbase(I1_0, 0);
-        int bytes = 0;  // the phase's slabs with their guards
-        for (int k = 0; k < ks; ++k) bytes += C::slab_bytes(I1_0 + k);
+        int bytes = 0;  // the phase's slabs with their guards; in the last layer (I1_0 = D) only the first slab exists
+        for (int k = 0; k < ks; ++k)
+            if (I1_0 + k <= S::D) bytes += C::slab_bytes(I1_0 + k);
+        if (bytes == 0) continue;  // uniform over the cluster: no slab, nothing to compute or flush
         uint8_t* slab0 = sSlab + (goff & 15);  // sSlab[0] <-> Delta offset goff & ~15
         uint8_t* dummy = sSlab + qround16(C::SLAB) + (tid & 15);  // sink for the stores of non-exponents
         const int TP2 = (T + 1) >> 1;

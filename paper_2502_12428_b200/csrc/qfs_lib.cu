@@ -144,6 +144,16 @@ __global__ void __launch_bounds__(1024) k_compact(const int8_t* __restrict__ hei
     if (tid == 0) *count = s_base;
 }
 
+// M (uint8, row pitch `pitch`) -> the reference's entry block: uint16 little-endian, row-major n x n
+// (mtsmatrix.py:350-365 matrix_to_bytes, MtsMatrix.entries is uint16, mtsmatrix.py:96)
+__global__ void k_widen_u16(const uint8_t* __restrict__ M, int n, int pitch, uint16_t* __restrict__ out)
+{
+    const int r = blockIdx.x;
+    const uint8_t* src = M + (size_t)blockIdx.y * n * pitch + (size_t)r * pitch;
+    uint16_t* dst = out + ((size_t)blockIdx.y * n + r) * n;
+    for (int c = threadIdx.x; c < n; c += blockDim.x) dst[c] = src[c];
+}
+
 // heights[i] == -1 (pending) -> 0 (infinity); used when bound < 2 (height.py:126-127)
 __global__ void k_pending_to_inf(int8_t* heights, int B)
 {
@@ -234,7 +244,8 @@ int build_tables(qfs_ctx* ctx)
         ctx->staged_multi = ((int)items.size() != S::ngroups);
         ctx->n_items = (int)items.size();
         ctx->staged_bufwords = SC::ZW + max_staged + SC::VWORDS;
-        if (const char* e = getenv("QFS_STAGED_NBUF")) ctx->staged_nbuf = std::max(1, std::min(4, atoi(e)));
+        // One staging buffer per CTA: with the arrive/sync split of k_matrix_staged a consumer must not be able to
+        // run a quad ahead of the producer warp (more buffers would need one barrier per buffer).
         ctx->staged_smem = ctx->staged_nbuf * (size_t)ctx->staged_bufwords * 4;
         CU(ctx->items.reserve(items.size() * sizeof(PanelItem)));
         CU(cudaMemcpy(ctx->items.ptr, items.data(), items.size() * sizeof(PanelItem), cudaMemcpyHostToDevice));
@@ -593,6 +604,35 @@ int run_stage_matrix(qfs_ctx* ctx, const uint8_t* delta, size_t B, uint8_t* M)
     return QFS_OK;
 }
 
+// Operator matrices of B quartics in the reference's export layout (uint16 entries, no pitch), host or device output.
+template <int P>
+int run_export_matrix(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, uint16_t* M16)
+{
+    using S = Shape<P>;
+    CU(cudaSetDevice(ctx->device));
+    CU(cudaMemsetAsync(ctx->flags.ptr, 0, 4 * sizeof(int), ctx->stream));
+    const bool out_dev = is_device_ptr(M16);
+    const size_t nn = (size_t)S::N * S::N;
+    const size_t slice = tap_slice<P>(ctx, B, per_surface_bytes<P>() + 2 * nn);
+    CU(ctx->tapA.reserve(slice * 35));
+    for (size_t done = 0; done < B; done += slice) {
+        const int cnt = (int)std::min(slice, B - done);
+        int rc = reserve_chunk<P>(ctx, (size_t)cnt);
+        if (rc) return rc;
+        uint16_t* d_out = M16 + done * nn;
+        if (!out_dev) { CU(ctx->tapB.reserve((size_t)cnt * nn * 2)); d_out = ctx->tapB.as<uint16_t>(); }
+        CU(cudaMemcpyAsync(ctx->tapA.ptr, coeffs + done * 35, (size_t)cnt * 35, cudaMemcpyDefault, ctx->stream));
+        if ((rc = launch_power_full<P>(ctx, ctx->tapA.as<uint8_t>(), nullptr, cnt, nullptr))) return rc;
+        if ((rc = launch_delta<P>(ctx, cnt))) return rc;
+        if ((rc = launch_matrix<P>(ctx, cnt, nullptr, nullptr))) return rc;
+        k_widen_u16<<<dim3(S::N, cnt), 256, 0, ctx->stream>>>(ctx->M.as<uint8_t>(), S::N, S::pitch, d_out);
+        CU(cudaGetLastError());
+        if (!out_dev) CU(cudaMemcpyAsync(M16 + done * nn, d_out, (size_t)cnt * nn * 2, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+    }
+    return check_device_flags(ctx);
+}
+
 template <int P>
 int run_stage_chain(qfs_ctx* ctx, const uint8_t* M, const uint8_t* v0, size_t B, int max_steps, uint8_t* trace,
                     int8_t* heights, int8_t* iters)
@@ -783,6 +823,26 @@ int qfs_stage_matrix(qfs_ctx* ctx, const uint8_t* delta, size_t B, uint8_t* M)
     if (B && (!delta || !M)) return fail(ctx, QFS_EINVAL, "NULL buffer");
     QFS_DISPATCH(ctx->p, run_stage_matrix<3>(ctx, delta, B, M), run_stage_matrix<5>(ctx, delta, B, M),
                  run_stage_matrix<7>(ctx, delta, B, M), run_stage_matrix<11>(ctx, delta, B, M), QFS_EINVAL)
+}
+
+int qfs_debug_fill_workspaces(qfs_ctx* ctx, int byte)
+{
+    if (!ctx) return QFS_EINVAL;
+    CU(cudaSetDevice(ctx->device));
+    DevBuf* bufs[] = {&ctx->g, &ctx->h, &ctx->A, &ctx->E, &ctx->delta, &ctx->M, &ctx->v1, &ctx->vacc, &ctx->tapA, &ctx->tapB,
+                      &ctx->coeffs, &ctx->heights, &ctx->iters, &ctx->list};
+    for (DevBuf* b : bufs)
+        if (b->ptr) CU(cudaMemsetAsync(b->ptr, byte, b->cap, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return QFS_OK;
+}
+
+int qfs_export_matrix(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, uint16_t* M16)
+{
+    if (!ctx) return QFS_EINVAL;
+    if (B && (!coeffs || !M16)) return fail(ctx, QFS_EINVAL, "NULL buffer");
+    QFS_DISPATCH(ctx->p, run_export_matrix<3>(ctx, coeffs, B, M16), run_export_matrix<5>(ctx, coeffs, B, M16),
+                 run_export_matrix<7>(ctx, coeffs, B, M16), run_export_matrix<11>(ctx, coeffs, B, M16), QFS_EINVAL)
 }
 
 int qfs_stage_matvec_chain(qfs_ctx* ctx, const uint8_t* M, const uint8_t* v0, size_t B, int max_steps, uint8_t* trace,

@@ -57,7 +57,7 @@ struct Shape {
     static constexpr int ZPAD = qround16(P * d + 1);       // leading zeros: covers offset p*(R-r3) <= p*d
     static constexpr int nruns = (D + 1) * (D + 2) / 2;
     static constexpr int Lg = ZPAD + L + G * nruns;
-    static constexpr int Lg_pad = qround16(Lg);
+    static constexpr int Lg_pad = (Lg + 31) & ~31;  // whole 128-byte staging units of the quad-interleaved array (qfs_matrix_staged.cuh)
     // Four surfaces (a "quad": slots 4q..4q+3 of a chunk) share one byte-interleaved Delta array:
     // byte x of slot s sits at (s>>2)*quad_stride + 4*x + (s&3), so one aligned 32-bit load fetches the
     // same Delta entry of the four surfaces (qfs_matrix.cuh gathers that way).

@@ -136,6 +136,19 @@ class Engine:
         self._check(self.lib.qfs_stage_matrix(self._h, dl.ctypes.data, B, out.ctypes.data))
         return out
 
+    def debug_fill_workspaces(self, byte):
+        """Test hook: overwrite every device workspace with `byte` (include/qfs.h)."""
+        self._check(self.lib.qfs_debug_fill_workspaces(self._h, int(byte)))
+
+    def export_matrix(self, coeffs):
+        """Operator matrices [B][N][N] as uint16, the reference's MtsMatrix.entries (mtsmatrix.py:96)."""
+        c = np.ascontiguousarray(coeffs, dtype=np.uint8).reshape(-1, 35)
+        B = c.shape[0]
+        n = self.shape.N
+        out = np.empty((B, n, n), dtype="<u2")
+        self._check(self.lib.qfs_export_matrix(self._h, c.ctypes.data, B, out.ctypes.data))
+        return out
+
     def stage_matvec_chain(self, M, v0, max_steps, trace=False):
         n = self.shape.N
         M = np.ascontiguousarray(M, dtype=np.uint8).reshape(-1, n, n)

