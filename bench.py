@@ -275,7 +275,7 @@ def gpu_line(args, p, res, world, with_cpu):
     value = world * batch * steps / (res["ms"] * 1e-3)
     stage = {k: v / steps for k, v in res["stage"].items()}
     kernels = {"delta": ("k_delta", stage["ms_delta"], ab["delta"]),
-               "matrix": ("k_matrix", stage["ms_matrix"], ab["matrix"]),
+               "matrix": ("k_matrix_staged", stage["ms_matrix"], ab["matrix"]),
                "matvec": ("k_chain", stage["ms_matvec"], ab["matvec"])}
     top = max(kernels, key=lambda k: kernels[k][1])
     name, kms, kbytes = kernels[top]
@@ -361,14 +361,25 @@ def main():
     if rank == 0:
         line = gpu_line(args, args.p, res, world, with_cpu=True)
     if not args.no_also and args.p == 5:
+        keep = ("value", "unit", "ms_per_step", "steps", "hard_per_s", "vs_baseline", "stage_ms_per_step", "roofline",
+                "roofline_pipeline", "e2e", "cpu_baseline", "height_histogram", "config")
         k7 = max(2, args.steps // 3)
         res7 = measure_gpu(7, args.batch, k7, 3, args.seed, rank, world, local, dist)
         res7["steps"] = k7
         if rank == 0:
             l7 = gpu_line(args, 7, res7, world, with_cpu=(world == 1))
-            keep = ("value", "unit", "ms_per_step", "steps", "hard_per_s", "vs_baseline", "stage_ms_per_step", "roofline",
-                    "roofline_pipeline", "e2e", "cpu_baseline", "height_histogram")
             line["also"] = {"F_7": {k: l7[k] for k in keep if k in l7}}
+        # BASELINE.json configs[4]: F_11 (12341 x 12341 operator, 152 MB per matrix): a batch sized so that its
+        # ~9% hard surfaces fill one HBM-budgeted chunk; no CPU arm (the oracle needs minutes per F_11 surface)
+        b11 = min(args.batch, 4000)
+        saved = args.batch
+        args.batch = b11
+        res11 = measure_gpu(11, b11, 2, 3, args.seed, rank, world, local, dist)
+        res11["steps"] = 2
+        if rank == 0:
+            l11 = gpu_line(args, 11, res11, world, with_cpu=False)
+            line["also"]["F_11"] = {k: l11[k] for k in keep if k in l11}
+        args.batch = saved
     if rank == 0:
         print(json.dumps(line))
     if dist is not None:

@@ -75,7 +75,7 @@ typedef struct qfs_stats {
 
 int qfs_version(void);
 
-/* 0 if p is supported by this build (3, 5, 7, 11); fills *out when non-NULL. */
+/* 0 if p is supported by this build (3, 5, 7, 11, 13); fills *out when non-NULL. */
 int qfs_get_shape(int p, qfs_shape *out);
 
 /* Per-(p, device) context: index tables, workspaces, streams.

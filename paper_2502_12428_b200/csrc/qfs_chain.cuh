@@ -67,7 +67,15 @@ k_chain(const uint8_t* __restrict__ M_all, const uint8_t* __restrict__ v0_all, c
         {
             const uint4* src = reinterpret_cast<const uint4*>(v0_all + (size_t)slot * S::pitch);
             for (int i = tid; i < NCH; i += C::NT) {
-                reinterpret_cast<uint4*>(va)[i] = src[i];
+                uint4 x = src[i];
+                if (i == NCH - 1 && S::pitch != S::N) {  // the pad bytes of v1 are never written by the builder: mask them
+                    uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                    for (int b = 0; b < 16; ++b)
+                        if (16 * (NCH - 1) + b >= S::N) w[b >> 2] &= ~(0xFFu << (8 * (b & 3)));
+                    x = make_uint4(w[0], w[1], w[2], w[3]);
+                }
+                reinterpret_cast<uint4*>(va)[i] = x;
                 reinterpret_cast<uint4*>(vb)[i] = make_uint4(0, 0, 0, 0);
             }
         }

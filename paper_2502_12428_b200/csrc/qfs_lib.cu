@@ -14,6 +14,7 @@
 #include "../../include/qfs.h"
 #include "qfs_chain.cuh"
 #include "qfs_delta.cuh"
+#include "qfs_delta_direct.cuh"
 #include "qfs_matrix.cuh"
 #include "qfs_matrix_staged.cuh"
 #include "qfs_power.cuh"
@@ -74,6 +75,7 @@ struct qfs_ctx {
     int staged_bufwords = 0;
     int staged_nbuf = 1;
     int staged_multi = 0;
+    int delta_direct = 0;                           // QFS_DELTA_DIRECT: use k_delta_direct for every prime (cross-check)
     int staged_nocopy = 0;                          // QFS_STAGED_NOCOPY: measurement aid (skips the staging copies; results are garbage)
     int matrix_version = 6;                         // 6 = shared-memory staged builder, 4 = direct gather (QFS_MATRIX_V)
     int* h_flags = nullptr;                         // pinned mirror of flags
@@ -256,7 +258,10 @@ int build_tables(qfs_ctx* ctx)
     }
     CU(cudaFuncSetAttribute(k_fedder<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, PowerCfg<P>::FED_SMEM));
     CU(cudaFuncSetAttribute(k_power_full<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, PowerCfg<P>::FULL_SMEM));
-    CU(cudaFuncSetAttribute(k_delta<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, DeltaCfg<P>::SMEM));
+    if constexpr (DeltaCfg<P>::SMEM <= 227 * 1024)
+        CU(cudaFuncSetAttribute(k_delta<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, DeltaCfg<P>::SMEM));
+    CU(cudaFuncSetAttribute(k_delta_direct<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, DeltaDirectCfg<P>::SMEM));
+    ctx->delta_direct = getenv("QFS_DELTA_DIRECT") ? 1 : 0;
     CU(cudaFuncSetAttribute(k_chain<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, ChainCfg<P>::SMEM));
     return QFS_OK;
 }
@@ -299,10 +304,25 @@ int launch_power_full(qfs_ctx* ctx, const uint8_t* d_coeffs, const uint32_t* d_l
 template <int P>
 int launch_delta(qfs_ctx* ctx, int count)
 {
-    k_delta<P><<<4 * ((count + 3) / 4), DeltaCfg<P>::NT, DeltaCfg<P>::SMEM, ctx->stream>>>(ctx->h.as<uint8_t>(), ctx->A.as<uint8_t>(),
-                                                                          ctx->E.as<uint8_t>(), ctx->delta.as<uint8_t>(), count);
-    ctx->stats.kernel_launches++;
-    CU(cudaGetLastError());
+    using S = Shape<P>;
+    if (DeltaCfg<P>::SMEM > 227 * 1024 || ctx->delta_direct) {
+        // the slab of k_delta does not fit (p = 13), or QFS_DELTA_DIRECT asks for the cross-check kernel
+        const size_t quads = ((size_t)count + 3) / 4;
+        CU(cudaMemsetAsync(ctx->delta.ptr, 0, quads * S::quad_stride, ctx->stream));
+        const dim3 grid(DeltaDirectCfg<P>::NBLK, (unsigned)count);
+        k_delta_direct<P><<<grid, DeltaDirectCfg<P>::NT, DeltaDirectCfg<P>::SMEM, ctx->stream>>>(
+            ctx->h.as<uint8_t>(), ctx->A.as<uint8_t>(), ctx->E.as<uint8_t>(), ctx->unrank.as<uint32_t>() + qunrank_offset(P - 1),
+            ctx->delta.as<uint8_t>(), count);
+        ctx->stats.kernel_launches++;
+        CU(cudaGetLastError());
+        return QFS_OK;
+    }
+    if constexpr (DeltaCfg<P>::SMEM <= 227 * 1024) {
+        k_delta<P><<<4 * ((count + 3) / 4), DeltaCfg<P>::NT, DeltaCfg<P>::SMEM, ctx->stream>>>(ctx->h.as<uint8_t>(), ctx->A.as<uint8_t>(),
+                                                                              ctx->E.as<uint8_t>(), ctx->delta.as<uint8_t>(), count);
+        ctx->stats.kernel_launches++;
+        CU(cudaGetLastError());
+    }
     return QFS_OK;
 }
 
@@ -677,13 +697,14 @@ void fill_shape(qfs_shape* s)
     s->p = P; s->d = S::d; s->D = S::D; s->N = S::N; s->pitch = S::pitch; s->cap = S::cap; s->L = S::L;
 }
 
-#define QFS_DISPATCH(p, expr3, expr5, expr7, expr11, bad) \
-    switch (p) {                                          \
-        case 3: return expr3;                             \
-        case 5: return expr5;                             \
-        case 7: return expr7;                             \
-        case 11: return expr11;                           \
-        default: return bad;                              \
+#define QFS_FOR_PRIME(p, F, ...)                 \
+    switch (p) {                                 \
+        case 3: return F<3>(__VA_ARGS__);        \
+        case 5: return F<5>(__VA_ARGS__);        \
+        case 7: return F<7>(__VA_ARGS__);        \
+        case 11: return F<11>(__VA_ARGS__);      \
+        case 13: return F<13>(__VA_ARGS__);      \
+        default: return QFS_EINVAL;              \
     }
 
 }  // namespace
@@ -701,6 +722,7 @@ int qfs_get_shape(int p, qfs_shape* out)
         case 5: fill_shape<5>(s); return QFS_OK;
         case 7: fill_shape<7>(s); return QFS_OK;
         case 11: fill_shape<11>(s); return QFS_OK;
+        case 13: fill_shape<13>(s); return QFS_OK;
         default: return QFS_EINVAL;
     }
 }
@@ -727,7 +749,7 @@ int qfs_create(int p, int device, size_t max_batch, qfs_ctx** out)
     if (!out) return fail(nullptr, QFS_EINVAL, "out is NULL");
     *out = nullptr;
     if (qfs_get_shape(p, nullptr) != QFS_OK)
-        return fail(nullptr, QFS_EINVAL, "p=%d is not supported by this build (supported: 3, 5, 7, 11)", p);
+        return fail(nullptr, QFS_EINVAL, "p=%d is not supported by this build (supported: 3, 5, 7, 11, 13)", p);
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);
     if (e != cudaSuccess || ndev == 0)
@@ -762,7 +784,8 @@ int qfs_create(int p, int device, size_t max_batch, qfs_ctx** out)
         case 3: rc = build_tables<3>(ctx); break;
         case 5: rc = build_tables<5>(ctx); break;
         case 7: rc = build_tables<7>(ctx); break;
-        default: rc = build_tables<11>(ctx); break;
+        case 11: rc = build_tables<11>(ctx); break;
+        default: rc = build_tables<13>(ctx); break;
     }
     if (rc) return bail(rc);
     *out = ctx;
@@ -795,34 +818,28 @@ int qfs_heights(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, int bound, int8_t
     if (!ctx) return QFS_EINVAL;
     if (B && (!coeffs || !heights || !iters)) return fail(ctx, QFS_EINVAL, "NULL buffer");
     if (bound < 1 || bound > 127) return fail(ctx, QFS_EINVAL, "bound must be in 1..127, got %d", bound);
-    QFS_DISPATCH(ctx->p, run_heights<3>(ctx, coeffs, B, bound, heights, iters, stream),
-                 run_heights<5>(ctx, coeffs, B, bound, heights, iters, stream),
-                 run_heights<7>(ctx, coeffs, B, bound, heights, iters, stream),
-                 run_heights<11>(ctx, coeffs, B, bound, heights, iters, stream), QFS_EINVAL)
+    QFS_FOR_PRIME(ctx->p, run_heights, ctx, coeffs, B, bound, heights, iters, stream)
 }
 
 int qfs_stage_power(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, uint8_t* g, uint8_t* fedder)
 {
     if (!ctx) return QFS_EINVAL;
     if (B && !coeffs) return fail(ctx, QFS_EINVAL, "NULL buffer");
-    QFS_DISPATCH(ctx->p, run_stage_power<3>(ctx, coeffs, B, g, fedder), run_stage_power<5>(ctx, coeffs, B, g, fedder),
-                 run_stage_power<7>(ctx, coeffs, B, g, fedder), run_stage_power<11>(ctx, coeffs, B, g, fedder), QFS_EINVAL)
+    QFS_FOR_PRIME(ctx->p, run_stage_power, ctx, coeffs, B, g, fedder)
 }
 
 int qfs_stage_delta(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, uint8_t* delta)
 {
     if (!ctx) return QFS_EINVAL;
     if (B && (!coeffs || !delta)) return fail(ctx, QFS_EINVAL, "NULL buffer");
-    QFS_DISPATCH(ctx->p, run_stage_delta<3>(ctx, coeffs, B, delta), run_stage_delta<5>(ctx, coeffs, B, delta),
-                 run_stage_delta<7>(ctx, coeffs, B, delta), run_stage_delta<11>(ctx, coeffs, B, delta), QFS_EINVAL)
+    QFS_FOR_PRIME(ctx->p, run_stage_delta, ctx, coeffs, B, delta)
 }
 
 int qfs_stage_matrix(qfs_ctx* ctx, const uint8_t* delta, size_t B, uint8_t* M)
 {
     if (!ctx) return QFS_EINVAL;
     if (B && (!delta || !M)) return fail(ctx, QFS_EINVAL, "NULL buffer");
-    QFS_DISPATCH(ctx->p, run_stage_matrix<3>(ctx, delta, B, M), run_stage_matrix<5>(ctx, delta, B, M),
-                 run_stage_matrix<7>(ctx, delta, B, M), run_stage_matrix<11>(ctx, delta, B, M), QFS_EINVAL)
+    QFS_FOR_PRIME(ctx->p, run_stage_matrix, ctx, delta, B, M)
 }
 
 int qfs_debug_fill_workspaces(qfs_ctx* ctx, int byte)
@@ -841,8 +858,7 @@ int qfs_export_matrix(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, uint16_t* M
 {
     if (!ctx) return QFS_EINVAL;
     if (B && (!coeffs || !M16)) return fail(ctx, QFS_EINVAL, "NULL buffer");
-    QFS_DISPATCH(ctx->p, run_export_matrix<3>(ctx, coeffs, B, M16), run_export_matrix<5>(ctx, coeffs, B, M16),
-                 run_export_matrix<7>(ctx, coeffs, B, M16), run_export_matrix<11>(ctx, coeffs, B, M16), QFS_EINVAL)
+    QFS_FOR_PRIME(ctx->p, run_export_matrix, ctx, coeffs, B, M16)
 }
 
 int qfs_stage_matvec_chain(qfs_ctx* ctx, const uint8_t* M, const uint8_t* v0, size_t B, int max_steps, uint8_t* trace,
@@ -850,10 +866,7 @@ int qfs_stage_matvec_chain(qfs_ctx* ctx, const uint8_t* M, const uint8_t* v0, si
 {
     if (!ctx) return QFS_EINVAL;
     if (B && (!M || !v0 || !heights || !iters)) return fail(ctx, QFS_EINVAL, "NULL buffer");
-    QFS_DISPATCH(ctx->p, run_stage_chain<3>(ctx, M, v0, B, max_steps, trace, heights, iters),
-                 run_stage_chain<5>(ctx, M, v0, B, max_steps, trace, heights, iters),
-                 run_stage_chain<7>(ctx, M, v0, B, max_steps, trace, heights, iters),
-                 run_stage_chain<11>(ctx, M, v0, B, max_steps, trace, heights, iters), QFS_EINVAL)
+    QFS_FOR_PRIME(ctx->p, run_stage_chain, ctx, M, v0, B, max_steps, trace, heights, iters)
 }
 
 }  // extern "C"

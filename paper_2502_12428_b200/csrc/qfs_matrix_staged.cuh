@@ -38,7 +38,7 @@ struct StagedCfg {
     using S = Shape<P>;
     static constexpr int V = (P >= 7) ? 2 : 1;                              // consecutive 32-bit words per thread (store width 4V bytes)
     static constexpr int TEAMS = V;                          // row teams
-    static constexpr int NT = (P >= 5) ? 256 : 64;           // consumer threads
+    static constexpr int NT = (P >= 13) ? 384 : (P >= 5 ? 256 : 64);  // consumer threads (p = 13: block c1 = 0 alone is 154 word groups)
     static constexpr int TEAM = NT / TEAMS;                  // threads (= word groups) per team
     static constexpr int NTL = NT + 32;                      // launched: + the producer warp
     static constexpr int WORDS = S::pitch / 4;
@@ -49,7 +49,7 @@ struct StagedCfg {
     static constexpr int SLICE = (P >= 11) ? 8 : (P >= 7 ? 8 : 16);        // quads per CTA
     static constexpr int ZW = (P * S::d + 4 + 3) & ~3;       // zero region (entries) read by columns that never match
     static constexpr int MAXC = S::d + 2;                    // pieces per panel
-    static constexpr int BUDGET = (P >= 11) ? 20480 : 12800; // default staged entries (x4 bytes) per panel
+    static constexpr int BUDGET = (P >= 13) ? 36864 : (P >= 11 ? 20480 : 12800);  // default staged entries (x4 bytes) per panel
     static constexpr size_t MSTRIDE = (size_t)S::N * S::pitch;
     static constexpr int VSEG = MAXG * 4 * V + 16;           // bytes of one surface's slice of v0 staged per buffer (16-byte aligned window)
     static constexpr int VWORDS = 4 * VSEG / 4;              // 32-bit words of the v0 area at the end of a buffer

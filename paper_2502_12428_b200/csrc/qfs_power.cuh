@@ -48,7 +48,7 @@ template <int P>
 struct PowerCfg {
     using S = Shape<P>;
     static constexpr int J0 = (P - 1) / 2;              // last fully computed level of the Fedder chain
-    static constexpr int FED_WARPS = 8;                 // surfaces per CTA in k_fedder
+    static constexpr int FED_WARPS = (P >= 13) ? 4 : 8;  // surfaces per CTA in k_fedder (shared-memory bound at p = 13)
     static constexpr int FED_BUF = qround16(qc3(4 * J0 + 3));
     static constexpr int RB_DEG = 4 * P;                // row-base tables up to this degree
     static constexpr int FULL_NT = 256;

@@ -19,7 +19,7 @@ def shape_of(p):
     """qfs_shape for a supported prime (DomainError otherwise)."""
     s = _native.QfsShape()
     if _native.load().qfs_get_shape(int(p), ctypes.byref(s)) != 0:
-        raise DomainError(f"p={p} is not supported by the GPU engine (supported: 3, 5, 7, 11)")
+        raise DomainError(f"p={p} is not supported by the GPU engine (supported: 3, 5, 7, 11, 13)")
     return s
 
 

@@ -28,7 +28,7 @@ from .errors import DomainError
 from .quartic import NCOEFF, NVARS, coeff_vector
 
 INFINITE = math.inf
-SUPPORTED_PRIMES = (3, 5, 7, 11)
+SUPPORTED_PRIMES = (3, 5, 7, 11, 13)
 
 
 def is_prime(n: int) -> bool:

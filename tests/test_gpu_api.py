@@ -46,6 +46,41 @@ def test_f11_published_rows():
     assert [int(i) for i in its] == [r["height"] - 1 for r in rows]
 
 
+def test_f13_published_rows():
+    """The five F_13 rows of the published table (k3_tables.txt:30-34): 20825 x 20825 operator, 434 MB per surface,
+    Delta from k_delta_direct (the slab kernel does not fit shared memory at p = 13)."""
+    import paper_2502_12428_b200 as q
+    rows = [r for r in ROWS if r["p"] == 13]
+    hs, its = q.height_batch(13, np.array([r["coeffs"] for r in rows], dtype=np.uint8))
+    assert [int(h) for h in hs] == [r["height"] for r in rows]
+    assert [int(i) for i in its] == [r["height"] - 1 for r in rows]
+    # a seeded handful more: the distribution is ~1/13 hard, heights 1 and 2 only at this size
+    c = q.sample_block(13, 40, 3, 0)
+    hs, its = q.height_batch(13, c)
+    assert set(int(h) for h in hs) <= {1, 2, 3} and (hs == 1).sum() >= 30
+
+
+@pytest.mark.parametrize("p", [3, 5, 7, 11])
+def test_direct_witt_carry_kernel_equals_the_slab_kernel(p, monkeypatch):
+    """k_delta_direct (the p = 13 path) against k_delta on primes that have both: identical dense Delta and,
+    through the whole pipeline, identical heights."""
+    import paper_2502_12428_b200 as q
+    from paper_2502_12428_b200.engine import Engine, get_engine
+    c = q.sample_block(p, 6 if p < 11 else 2, 21, 0)
+    want = get_engine(p, 0).stage_delta(c)
+    monkeypatch.setenv("QFS_DELTA_DIRECT", "1")
+    eng = Engine(p, 0)
+    try:
+        got = eng.stage_delta(c)
+        assert np.array_equal(got, want)
+        big = q.sample_block(p, 300 if p < 11 else 30, 22, 0)
+        h1, i1 = eng.heights(big, 10)
+        h0, i0 = get_engine(p, 0).heights(big, 10)
+        assert np.array_equal(h1, h0) and np.array_equal(i1, i0)
+    finally:
+        eng.close()
+
+
 def test_run_search_on_gpu_matches_reference():
     import paper_2502_12428_b200 as q
     z = np.load(os.path.join(GOLDEN, "heights_p5_seed0_w0_10000.npz"))

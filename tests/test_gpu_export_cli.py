@@ -68,15 +68,18 @@ def test_cli_matrix_verify_bench(capsys, tmp_path):
     run(capsys, "matrix", "--p", "3", "--poly", fermat, "--out", str(bpath), "--format", "binary")
     assert q.matrix_from_text(tpath.read_text(), 4) == q.matrix_from_bytes(bpath.read_bytes())
     assert hashlib.sha256(bpath.read_bytes()).hexdigest() == GOLD["matrices"][0]["bytes_sha256"]
-    # verify: packaged table, every prime this build supports (F_13 rows are reported as skipped)
+    # verify: the whole packaged table, F_5 ... F_13 (the reference's extended acceptance set)
     rc, out, _ = run(capsys, "verify")
-    assert rc == 0 and "27 rows, 0 mismatches" in out and "5 rows skipped" in out
+    assert rc == 0 and "32 rows, 0 mismatches" in out
     fx = tmp_path / "fx.txt"
     fx.write_text("5 ; 2 ; " + fermat + "\n")            # wrong on purpose: Fermat over F_5 has height 1
     rc, out, _ = run(capsys, "verify", "--fixtures", str(fx))
     assert rc == 1 and "MISMATCH" in out
-    rc, out, _ = run(capsys, "verify", "--primes", "13")
-    assert rc == 3
+    fx.write_text("17 ; 1 ; " + fermat + "\n")            # a prime this build has no kernels for
+    rc, out, _ = run(capsys, "verify", "--fixtures", str(fx))
+    assert rc == 0 and "1 rows skipped" in out
+    rc, out, err = run(capsys, "height", "--p", "17", "--poly", fermat)
+    assert rc == 3 and "not supported" in err
     rc, out, _ = run(capsys, "height", "--p", "5", "--poly", fermat)
     assert rc == 0 and "height 1" in out and "iterations 0" in out
     for what in ("power", "mts", "matvec", "height"):
