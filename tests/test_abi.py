@@ -45,7 +45,9 @@ def test_unsupported_prime_is_a_domain_error():
     from paper_2502_12428_b200.engine import shape_of
     from paper_2502_12428_b200.errors import DomainError
     with pytest.raises(DomainError):
-        shape_of(13)
+        shape_of(17)
+    s13 = shape_of(13)
+    assert (s13.N, s13.d, s13.D, s13.L, s13.cap) == (20825, 48, 624, 40885625, 12076)
 
 
 def test_no_cpu_fallback():
