@@ -88,7 +88,7 @@ def test_batch_argument_checks_need_no_gpu():
     with pytest.raises(q.DomainError):
         q.height_batch(4, np.ones((3, 35), np.uint8))
     with pytest.raises(q.DomainError):
-        q.height_batch(13, np.ones((3, 35), np.uint8))
+        q.height_batch(17, np.ones((3, 35), np.uint8))
     with pytest.raises(q.DomainError):
         q.height_batch(5, np.ones((3, 35), np.uint8), bound=0)
 
