@@ -7,8 +7,10 @@
 // dot product is at most N (p-1)^2 <= 12341 * 100 < 2^31, so ONE reduction per row is exact:
 // uint8 x uint8 products are summed four at a time with DP4A into a 32-bit accumulator.
 //
-// Mapping.  Persistent CTAs pull surfaces from a global queue (early exit makes the work per
-// surface vary from 1 to bound-1 passes over M).  The vector lives in shared memory (ping-pong);
+// Mapping.  Persistent CTAs (1024 threads) pull surfaces from a global queue (early exit makes the work per
+// surface vary from 1 to bound-1 passes over M).  The kernel is a latency-bound stream: what matters is the
+// number of 16-byte loads in flight per SM (measured, F_5 / F_7 / F_11 stage ms: 512 threads x 4 rows x 2 CTAs
+// 1.45 / 6.9 / 13.3; 1024 x 4 x 2 0.81 / 3.65 / 8.6; 1024 x 8 x 1 1.10 / 4.44 / 4.1).  The vector lives in shared memory (ping-pong);
 // each warp owns UNROLL rows at a time, lanes stream 16-byte pieces of those rows from HBM with
 // non-allocating loads, and a warp-shuffle tree finishes each dot product.
 #pragma once
@@ -17,8 +19,9 @@
 template <int P>
 struct ChainCfg {
     using S = Shape<P>;
-    static constexpr int NT = 512;
-    static constexpr int UNROLL = 4;
+    static constexpr int NT = 1024;
+    static constexpr int UNROLL = (P >= 11) ? 8 : 4;   // rows per warp pass: 16-byte loads in flight per lane
+    static constexpr int CTAS_PER_SM = (P >= 11) ? 1 : 2;  // p <= 7: 64 warps per SM (32 registers); p >= 11: few, long surfaces -> more loads per CTA
     static constexpr int SMEM = 2 * S::pitch;
 };
 
@@ -32,7 +35,7 @@ __device__ __forceinline__ uint4 ld_stream16(const uint4* p)
 }
 
 template <int P>
-__global__ void __launch_bounds__(ChainCfg<P>::NT)
+__global__ void __launch_bounds__(ChainCfg<P>::NT, ChainCfg<P>::CTAS_PER_SM)
 k_chain(const uint8_t* __restrict__ M_all, const uint8_t* __restrict__ v0_all, const uint32_t* __restrict__ list,
         int count, int start_it, int max_steps, uint8_t* __restrict__ trace, int8_t* __restrict__ heights,
         int8_t* __restrict__ iters, int* __restrict__ queue)

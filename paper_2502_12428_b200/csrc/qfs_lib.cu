@@ -378,7 +378,7 @@ int launch_chain(qfs_ctx* ctx, const uint8_t* v0, const uint32_t* d_list, int co
 {
     int* d_queue = ctx->flags.as<int>() + 1;
     CU(cudaMemsetAsync(d_queue, 0, sizeof(int), ctx->stream));
-    const int grid = std::min(count, ctx->sm_count * 2);
+    const int grid = std::min(count, ctx->sm_count * ChainCfg<P>::CTAS_PER_SM);
     k_chain<P><<<grid, ChainCfg<P>::NT, ChainCfg<P>::SMEM, ctx->stream>>>(ctx->M.as<uint8_t>(), v0, d_list, count, start_it,
                                                                         max_steps, trace, heights, iters, d_queue);
     ctx->stats.kernel_launches++;
