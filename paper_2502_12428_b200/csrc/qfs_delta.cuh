@@ -45,6 +45,12 @@ __device__ __forceinline__ void transpose4x4(const uint32_t (&in)[4], uint32_t (
     out[3] = __byte_perm(t2, t3, 0x7632);
 }
 
+// predicated byte store to shared memory (one ISETP + one @P STS; a select between two generic pointers costs three)
+__device__ __forceinline__ void st_shared_u8_le(uint32_t addr, uint32_t v, int a, int b)  // store if a <= b
+{
+    asm volatile("{\n.reg .pred q;\nsetp.le.s32 q, %2, %3;\n@q st.shared.u8 [%0], %1;\n}\n" ::"r"(addr), "r"(v), "r"(a), "r"(b) : "memory");
+}
+
 template <int P>
 struct DeltaCfg {
     using S = Shape<P>;
@@ -147,9 +153,9 @@ k_delta(const uint8_t* __restrict__ h_all, const uint8_t* __restrict__ A_all, co
             rbh[e] = (u1 + u2 <= S::dh) ? (uint16_t)qrowbase(S::dh, u1, u2) : (uint16_t)0;
         }
     }
-    // class table: sEc[c][w] byte b = -E[rho + p*t_j] mod p, j = 4w+b, taps ordered by |t| then lex; 0 outside deg 4p
-    for (int e = tid; e < (live ? C::NCLS * C::NWORD : 0); e += C::NT) {
-        const int c = e / C::NWORD, w = e - c * C::NWORD;
+    // class table: sEc[c][w] byte b = -E[rho + p*t_j] mod p, j = 4w+b, taps ordered by |t| then lex; 0 outside deg 4p.
+    // One thread per class walks the 35 taps once (the loops are unrolled: tap offsets are immediates).
+    for (int c = tid; c < (live ? C::NCLS : 0); c += C::NT) {
         const int rho1 = c / (P * P), rho2 = (c / P) % P, rho3 = c % P;
         uint32_t word = 0;
         int j = 0;
@@ -160,16 +166,15 @@ k_delta(const uint8_t* __restrict__ h_all, const uint8_t* __restrict__ A_all, co
 #pragma unroll
                 for (int t2 = 0; t2 <= k - t1; ++t2) {
                     const int t3 = k - t1 - t2;
-                    if ((j >> 2) == w) {
-                        const int J1 = rho1 + P * t1, J2 = rho2 + P * t2, J3 = rho3 + P * t3;
-                        if (J1 + J2 + J3 <= S::dE) {
-                            const uint32_t ev = gE[qrowbase(S::dE, J1, J2) + J3];
-                            word |= (ev ? (uint32_t)P - ev : 0u) << (8 * (j & 3));  // -E mod p: sums stay non-negative
-                        }
+                    const int J1 = rho1 + P * t1, J2 = rho2 + P * t2, J3 = rho3 + P * t3;
+                    if (J1 + J2 + J3 <= S::dE) {
+                        const uint32_t ev = gE[qrowbase(S::dE, J1, J2) + J3];
+                        word |= (ev ? (uint32_t)P - ev : 0u) << (8 * (j & 3));  // -E mod p: sums stay non-negative
                     }
+                    if ((j & 3) == 3) { sEc[c * C::NWORD + (j >> 2)] = word; word = 0; }
                     ++j;
                 }
-        sEc[e] = word;
+        sEc[c * C::NWORD + 8] = word;  // taps 32..34
     }
     __syncthreads();
     if (C::USE_BOX && live) {
@@ -230,19 +235,19 @@ k_delta(const uint8_t* __restrict__ h_all, const uint8_t* __restrict__ A_all, co
             if (I1_0 + k <= S::D) bytes += C::slab_bytes(I1_0 + k);
         if (bytes == 0) continue;  // uniform over the cluster: no slab, nothing to compute or flush
         uint8_t* slab0 = sSlab + (goff & 15);  // sSlab[0] <-> Delta offset goff & ~15
-        uint8_t* dummy = sSlab + qround16(C::SLAB) + (tid & 15);  // sink for the stores of non-exponents
         const int TP2 = (T + 1) >> 1;
         const float invT = 1.0f / (float)TP2;
+        const int sl_a = S::D - I1_0 + 1, sl_b = S::D - I1_0 + 2 + 2 * S::G;
+        const int sl_ab = sl_a * sl_b, sl_apb = sl_a + sl_b;
         for (int i = tid; i < (live ? ks * P * TP2 : 0); i += C::NT) {
             const int c = (int)(((float)i + 0.5f) * invT);  // = slab-in-phase * P + rho2
             const int jq = i - c * TP2;
             const int k = (c * ((65536 + P - 1) / P)) >> 16, rho2 = c - k * P;
             const int rho1 = rho1_0 + k;
             const int n = S::D - I1_0 - k;
-            uint8_t* slab = slab0;
-#pragma unroll
-            for (int kk = 0; kk < C::KS - 1; ++kk)
-                if (kk < k) slab += C::slab_bytes(I1_0 + kk);
+            // bytes of the k slabs in front of this one: sum_{kk<k} (a-kk)(b-kk)/2 with a = n0+1, b = n0+2+2G
+            // (slab_bytes(I) = (n+1)(n+2+2G)/2, n = D-I), in closed form: no per-item loop over the slabs
+            uint8_t* slab = slab0 + ((k * sl_ab - sl_apb * ((k * (k - 1)) >> 1) + ((k - 1) * k * (2 * k - 1)) / 6) >> 1);
             const uint32_t* ec = sEc + ((rho1 * P + rho2) * P) * C::NWORD;
             const uint32_t* hpq = sHp + 2 * jq;
             const int rs12 = rho1 + rho2;
@@ -268,13 +273,12 @@ k_delta(const uint8_t* __restrict__ h_all, const uint8_t* __restrict__ A_all, co
                 }
                 // rho3 <= room are real exponents (I4 >= 0); the odd point of a last pair does not exist
                 const int room = (2 * jq + u < T) ? n2 - P * s3 : -1;
-                uint8_t* out = slab + ((I2 * (2 * n + 3 - I2)) >> 1) + S::G * I2 + (n2 - P * s3);  // position of rho3 = 0
+                const uint32_t out32 = (uint32_t)__cvta_generic_to_shared(slab) + ((I2 * (2 * n + 3 - I2)) >> 1) + S::G * I2 + (n2 - P * s3);  // position of rho3 = 0
 #pragma unroll
                 for (int rho3 = 0; rho3 < P; ++rho3) {
                     // acc < 35 p (p-1) + p < 2^32 / p: the quotient by the magic multiply is exact
                     const uint32_t qq = __umulhi(acc[u][rho3], (uint32_t)(0xFFFFFFFFu / P + 1));
-                    uint8_t* o = (rho3 <= room) ? out - rho3 : dummy;
-                    *o = (uint8_t)(acc[u][rho3] - qq * (uint32_t)P);
+                    st_shared_u8_le(out32 - rho3, acc[u][rho3] - qq * (uint32_t)P, rho3, room);
                 }
             }
         }
