@@ -230,24 +230,24 @@ k_delta(const uint8_t* __restrict__ h_all, const uint8_t* __restrict__ A_all, co
         const int ks = min(C::KS, P - rho1_0);
         const int I1_0 = I1 + rho1_0;
         const int goff = S::gbase(I1_0, 0);
-        int bytes = 0;  // the phase's slabs with their guards; in the last layer (I1_0 = D) only the first slab exists
-        for (int k = 0; k < ks; ++k)
-            if (I1_0 + k <= S::D) bytes += C::slab_bytes(I1_0 + k);
+        // bytes of the phase's slabs with their guards; in the last layer (I1_0 = D) only the first slab exists.
+        // slab_bytes(I) = (n+1)(n+2+2G)/2 with n = D-I, so the bytes of the first k slabs are a cubic in k.
+        const int sl_a = S::D - I1_0 + 1, sl_b = S::D - I1_0 + 2 + 2 * S::G;
+        const int sl_ab = sl_a * sl_b, sl_apb = sl_a + sl_b;
+        auto slabs_before = [&](int k) { return (k * sl_ab - sl_apb * ((k * (k - 1)) >> 1) + ((k - 1) * k * (2 * k - 1)) / 6) >> 1; };
+        const int bytes = slabs_before(max(0, min(ks, S::D - I1_0 + 1)));
         if (bytes == 0) continue;  // uniform over the cluster: no slab, nothing to compute or flush
         uint8_t* slab0 = sSlab + (goff & 15);  // sSlab[0] <-> Delta offset goff & ~15
         const int TP2 = (T + 1) >> 1;
         const float invT = 1.0f / (float)TP2;
-        const int sl_a = S::D - I1_0 + 1, sl_b = S::D - I1_0 + 2 + 2 * S::G;
-        const int sl_ab = sl_a * sl_b, sl_apb = sl_a + sl_b;
         for (int i = tid; i < (live ? ks * P * TP2 : 0); i += C::NT) {
             const int c = (int)(((float)i + 0.5f) * invT);  // = slab-in-phase * P + rho2
             const int jq = i - c * TP2;
             const int k = (c * ((65536 + P - 1) / P)) >> 16, rho2 = c - k * P;
             const int rho1 = rho1_0 + k;
             const int n = S::D - I1_0 - k;
-            // bytes of the k slabs in front of this one: sum_{kk<k} (a-kk)(b-kk)/2 with a = n0+1, b = n0+2+2G
-            // (slab_bytes(I) = (n+1)(n+2+2G)/2, n = D-I), in closed form: no per-item loop over the slabs
-            uint8_t* slab = slab0 + ((k * sl_ab - sl_apb * ((k * (k - 1)) >> 1) + ((k - 1) * k * (2 * k - 1)) / 6) >> 1);
+            // bytes of the k slabs in front of this one, in closed form: no per-item loop over the slabs
+            uint8_t* slab = slab0 + slabs_before(k);
             const uint32_t* ec = sEc + ((rho1 * P + rho2) * P) * C::NWORD;
             const uint32_t* hpq = sHp + 2 * jq;
             const int rs12 = rho1 + rho2;
