@@ -38,7 +38,7 @@ struct StagedCfg {
     using S = Shape<P>;
     static constexpr int V = (P >= 7) ? 2 : 1;                              // consecutive 32-bit words per thread (store width 4V bytes)
     static constexpr int TEAMS = V;                          // row teams
-    static constexpr int NT = (P >= 13) ? 384 : (P >= 5 ? 256 : 64);  // consumer threads (p = 13: block c1 = 0 alone is 154 word groups)
+    static constexpr int NT = (P >= 13) ? 384 : (P == 7 ? 192 : (P >= 5 ? 256 : 64));  // consumer threads (p = 13: block c1 = 0 alone is 154 word groups; p = 7: 96-thread teams fit its ~91-group panels)
     static constexpr int TEAM = NT / TEAMS;                  // threads (= word groups) per team
     static constexpr int NTL = NT + 32;                      // launched: + the producer warp
     static constexpr int WORDS = S::pitch / 4;
