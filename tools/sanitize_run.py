@@ -1,0 +1,24 @@
+#!/usr/bin/env python3
+"""Small run for compute-sanitizer: every kernel of the pipeline, the stage taps and the export, for a few primes.
+
+    compute-sanitizer --tool memcheck  python tools/sanitize_run.py
+    compute-sanitizer --tool racecheck python tools/sanitize_run.py
+"""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2502_12428_b200 as q  # noqa: E402
+from paper_2502_12428_b200.engine import get_engine  # noqa: E402
+
+primes = [int(x) for x in sys.argv[1].split(",")] if len(sys.argv) > 1 else [3, 5, 7]
+for p in primes:
+    eng = get_engine(p, 0)
+    n = {3: 200, 5: 150, 7: 60}.get(p, 14)
+    c = q.sample_block(p, n, 7, 0)
+    hs, its = eng.heights(c, 10)
+    d = eng.stage_delta(c[:3])
+    m = eng.export_matrix(c[:2])
+    print(p, np.bincount(hs.astype(np.int64)).tolist(), d.shape, m.shape, flush=True)
