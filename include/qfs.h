@@ -104,6 +104,17 @@ int qfs_heights(qfs_ctx *ctx, const uint8_t *coeffs, size_t B, int bound,
                 int8_t *heights, int8_t *iters, void *stream);
 int qfs_get_stats(const qfs_ctx *ctx, qfs_stats *out);
 
+/* The same heights and iteration counts by the polynomial iteration, without
+ * Delta_1(f^(p-1)) and without the operator matrix: the on-device counterpart of
+ * the reference's cross-check height_naive (height.py:97-116),
+ *     g <- u(Delta * g),   computed as   g <- -f^(p-2) * u(Delta_1(f) * g)
+ * (csrc/qfs_free.cuh; valid because g[cap] = 0 inside the loop).  Same
+ * arguments and semantics as qfs_heights.  It is NOT the path the roofline of
+ * this library is quoted on (that path builds and streams M, like the
+ * reference's height_matrix); it exists to cross-check it and as a fast mode. */
+int qfs_heights_free(qfs_ctx *ctx, const uint8_t *coeffs, size_t B, int bound,
+                     int8_t *heights, int8_t *iters, void *stream);
+
 /* ---- stage taps (parity against the reference's intermediates) ----------
  * All taps run the SAME kernels as qfs_heights on every input row (no
  * height-1 shortcut) and write the reference's layouts. */

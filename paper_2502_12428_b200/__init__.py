@@ -7,7 +7,7 @@ raise EngineUnavailableError.
 """
 from .errors import DomainError, EngineUnavailableError, InternalInvariantError, ParseError, QfsplitError
 from .height import (INFINITE, HeightResult, SurfaceProblem, default_bound, height_batch, height_matrix,
-                     height_of_coeffs, is_prime)
+                     height_naive, height_of_coeffs, is_prime)
 from .mtsmatrix import (MtsMatrix, build_mts, build_mts_batch, matrix_from_bytes, matrix_from_text, matrix_to_bytes,
                         matrix_to_text, target_degree)
 from .quartic import Quartic, coeff_vector, parse_poly, poly_to_text
@@ -27,7 +27,7 @@ def fixtures_path() -> str:
 __all__ = [
     "DomainError", "EngineUnavailableError", "InternalInvariantError", "ParseError", "QfsplitError",
     "INFINITE", "HeightResult", "SurfaceProblem", "default_bound", "height_batch", "height_matrix",
-    "height_of_coeffs", "is_prime", "Quartic", "coeff_vector", "parse_poly", "poly_to_text",
+    "height_naive", "height_of_coeffs", "is_prime", "Quartic", "coeff_vector", "parse_poly", "poly_to_text",
     "FixtureRow", "FixtureVerdict", "FoundSurface", "HeightHistogram", "SearchConfig", "found_surfaces_text",
     "histogram_text", "parse_fixtures", "run_search", "sample_block", "sample_surface", "spectrum_rows",
     "spectrum_search", "verify_fixtures", "fixtures_path",

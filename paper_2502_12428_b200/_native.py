@@ -19,7 +19,7 @@ QFS_OK, QFS_EINVAL, QFS_ECUDA, QFS_EINVARIANT, QFS_ENOMEM = 0, -1, -2, -3, -4
 
 EXPORTS = (
     "qfs_version", "qfs_get_shape", "qfs_create", "qfs_destroy", "qfs_last_error",
-    "qfs_set_workspace_limit", "qfs_set_chunk", "qfs_heights", "qfs_get_stats",
+    "qfs_set_workspace_limit", "qfs_set_chunk", "qfs_heights", "qfs_heights_free", "qfs_get_stats",
     "qfs_stage_power", "qfs_stage_delta", "qfs_stage_matrix", "qfs_stage_matvec_chain",
     "qfs_export_matrix", "qfs_debug_fill_workspaces",
 )
@@ -82,6 +82,7 @@ def load():
     lib.qfs_set_workspace_limit.argtypes = [vp, sz]
     lib.qfs_set_chunk.argtypes = [vp, sz]
     lib.qfs_heights.argtypes = [vp, u8p, sz, ctypes.c_int, i8p, i8p, vp]
+    lib.qfs_heights_free.argtypes = [vp, u8p, sz, ctypes.c_int, i8p, i8p, vp]
     lib.qfs_get_stats.argtypes = [vp, ctypes.POINTER(QfsStats)]
     lib.qfs_stage_power.argtypes = [vp, u8p, sz, u8p, u8p]
     lib.qfs_stage_delta.argtypes = [vp, u8p, sz, u8p]

@@ -15,6 +15,7 @@
 #include "qfs_chain.cuh"
 #include "qfs_delta.cuh"
 #include "qfs_delta_direct.cuh"
+#include "qfs_free.cuh"
 #include "qfs_matrix.cuh"
 #include "qfs_matrix_staged.cuh"
 #include "qfs_power.cuh"
@@ -261,6 +262,7 @@ int build_tables(qfs_ctx* ctx)
     if constexpr (DeltaCfg<P>::SMEM <= 227 * 1024)
         CU(cudaFuncSetAttribute(k_delta<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, DeltaCfg<P>::SMEM));
     CU(cudaFuncSetAttribute(k_delta_direct<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, DeltaDirectCfg<P>::SMEM));
+    CU(cudaFuncSetAttribute(k_free<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, FreeCfg<P>::SMEM));
     ctx->delta_direct = getenv("QFS_DELTA_DIRECT") ? 1 : 0;
     CU(cudaFuncSetAttribute(k_chain<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, ChainCfg<P>::SMEM));
     return QFS_OK;
@@ -285,6 +287,18 @@ int reserve_chunk(qfs_ctx* ctx, size_t cap)
     CU(ctx->delta.reserve(cap * (size_t)S::Lg_pad));
     CU(ctx->M.reserve(cap * (size_t)S::N * S::pitch));
     CU(ctx->v1.reserve(cap * S::pitch));
+    return QFS_OK;
+}
+
+template <int P>
+int reserve_chunk_free(qfs_ctx* ctx, size_t cap)
+{
+    using S = Shape<P>;
+    cap = (cap + 3) & ~(size_t)3;
+    CU(ctx->g.reserve(cap * S::pitch));
+    CU(ctx->A.reserve(cap * S::pitch));
+    CU(ctx->h.reserve(cap * S::Nh_pad));
+    CU(ctx->E.reserve(cap * S::NE_pad));
     return QFS_OK;
 }
 
@@ -406,7 +420,7 @@ float elapsed(cudaEvent_t a, cudaEvent_t b)
 
 // ---- the pipeline ----------------------------------------------------------------------------
 template <int P>
-int run_heights(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, int bound, int8_t* heights, int8_t* iters, void* user_stream)
+int run_heights(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, int bound, int8_t* heights, int8_t* iters, void* user_stream, int matrix_free)
 {
     using S = Shape<P>;
     ctx->stats = qfs_stats{};
@@ -471,10 +485,11 @@ int run_heights(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, int bound, int8_t
             }
             limit = ctx->auto_limit;
         }
-        size_t cap = ctx->chunk_override ? ctx->chunk_override : std::max<size_t>(1, limit / per_surface_bytes<P>());
+        const size_t per = matrix_free ? (size_t)(3 * S::pitch + S::Nh_pad + S::NE_pad) : per_surface_bytes<P>();
+        size_t cap = ctx->chunk_override ? ctx->chunk_override : std::max<size_t>(1, limit / per);
         cap = std::min<size_t>(cap, (size_t)hard);
         while (true) {
-            int rc = reserve_chunk<P>(ctx, cap);
+            int rc = matrix_free ? reserve_chunk_free<P>(ctx, cap) : reserve_chunk<P>(ctx, cap);
             if (rc == QFS_OK) break;
             if (rc != QFS_ENOMEM || cap == 1) return rc;
             cudaGetLastError();
@@ -488,11 +503,22 @@ int run_heights(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, int bound, int8_t
             CU(cudaEventRecord(ctx->ev[0], ctx->stream));
             if ((rc = launch_power_full<P>(ctx, d_coeffs, d_list + done, cnt, nullptr))) return rc;
             CU(cudaEventRecord(ctx->ev[1], ctx->stream));
-            if ((rc = launch_delta<P>(ctx, cnt))) return rc;
-            CU(cudaEventRecord(ctx->ev[2], ctx->stream));
-            if ((rc = launch_matrix<P>(ctx, cnt, ctx->g.as<uint8_t>(), ctx->v1.as<uint8_t>()))) return rc;
-            CU(cudaEventRecord(ctx->ev[3], ctx->stream));
-            if ((rc = launch_chain<P>(ctx, ctx->v1.as<uint8_t>(), d_list + done, cnt, 1, bound - 1, nullptr, d_heights, d_iters))) return rc;
+            if (matrix_free) {
+                // the operator iteration without Delta and without M (qfs_free.cuh): stage times delta = matrix = 0
+                CU(cudaEventRecord(ctx->ev[2], ctx->stream));
+                CU(cudaEventRecord(ctx->ev[3], ctx->stream));
+                k_free<P><<<cnt, FreeCfg<P>::NT, FreeCfg<P>::SMEM, ctx->stream>>>(
+                    ctx->g.as<uint8_t>(), ctx->h.as<uint8_t>(), ctx->E.as<uint8_t>(), ctx->unrank.as<uint32_t>() + qunrank_offset(P),
+                    ctx->unrank.as<uint32_t>() + qunrank_offset(P - 1), d_list + done, bound - 1, d_heights, d_iters);
+                ctx->stats.kernel_launches++;
+                CU(cudaGetLastError());
+            } else {
+                if ((rc = launch_delta<P>(ctx, cnt))) return rc;
+                CU(cudaEventRecord(ctx->ev[2], ctx->stream));
+                if ((rc = launch_matrix<P>(ctx, cnt, ctx->g.as<uint8_t>(), ctx->v1.as<uint8_t>()))) return rc;
+                CU(cudaEventRecord(ctx->ev[3], ctx->stream));
+                if ((rc = launch_chain<P>(ctx, ctx->v1.as<uint8_t>(), d_list + done, cnt, 1, bound - 1, nullptr, d_heights, d_iters))) return rc;
+            }
             CU(cudaEventRecord(ctx->ev[4], ctx->stream));
             CU(cudaEventSynchronize(ctx->ev[4]));
             ctx->stats.ms_power += elapsed(ctx->ev[0], ctx->ev[1]);
@@ -818,7 +844,15 @@ int qfs_heights(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, int bound, int8_t
     if (!ctx) return QFS_EINVAL;
     if (B && (!coeffs || !heights || !iters)) return fail(ctx, QFS_EINVAL, "NULL buffer");
     if (bound < 1 || bound > 127) return fail(ctx, QFS_EINVAL, "bound must be in 1..127, got %d", bound);
-    QFS_FOR_PRIME(ctx->p, run_heights, ctx, coeffs, B, bound, heights, iters, stream)
+    QFS_FOR_PRIME(ctx->p, run_heights, ctx, coeffs, B, bound, heights, iters, stream, 0)
+}
+
+int qfs_heights_free(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, int bound, int8_t* heights, int8_t* iters, void* stream)
+{
+    if (!ctx) return QFS_EINVAL;
+    if (B && (!coeffs || !heights || !iters)) return fail(ctx, QFS_EINVAL, "NULL buffer");
+    if (bound < 1 || bound > 127) return fail(ctx, QFS_EINVAL, "bound must be in 1..127, got %d", bound);
+    QFS_FOR_PRIME(ctx->p, run_heights, ctx, coeffs, B, bound, heights, iters, stream, 1)
 }
 
 int qfs_stage_power(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, uint8_t* g, uint8_t* fedder)

@@ -81,7 +81,7 @@ class Engine:
         return st.as_dict()
 
     # -- hot path ----------------------------------------------------------------------------
-    def heights(self, coeffs, bound=10, out=None):
+    def heights(self, coeffs, bound=10, out=None, matrix_free=False):
         """(heights int8[B], iterations int8[B]); heights use 0 for infinity.
 
         coeffs: [B,35] uint8 numpy array or torch CUDA tensor.  With torch input the outputs are
@@ -108,7 +108,8 @@ class Engine:
         if _is_torch(coeffs):
             import torch
             stream = torch.cuda.current_stream(coeffs.device).cuda_stream
-        self._check(self.lib.qfs_heights(self._h, cptr, B, int(bound), hp, ip, stream))
+        fn = self.lib.qfs_heights_free if matrix_free else self.lib.qfs_heights
+        self._check(fn(self._h, cptr, B, int(bound), hp, ip, stream))
         del keep
         return hs, its
 

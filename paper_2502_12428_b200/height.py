@@ -13,8 +13,8 @@ plus the two batch entry points the reference only has as a loop body (search.py
     height_batch(p, coeffs[B,35], bound=10, devices=None) -> (heights int8[B], iterations int8[B])
 
 All heights are computed by libqfs.so on the GPU (EngineUnavailableError without it; there is no
-CPU fallback).  The reference's `height_naive` cross-check is not part of this path: the
-independent check of this package is the CPU oracle under oracle/, used by the tests only.
+CPU fallback).  `height_naive` (the reference's cross-check driver) is the matrix-free GPU iteration of
+csrc/qfs_free.cuh; the independent CPU check of this package is the oracle under oracle/, used by the tests only.
 """
 from __future__ import annotations
 
@@ -153,14 +153,21 @@ def split_blocks(total: int, parts: int):
     return out
 
 
-def height_batch(p: int, coeffs, bound: int = 10, devices=None):
+def height_batch(p: int, coeffs, bound: int = 10, devices=None, method: str = "matrix"):
     """Heights of B quartics given as rows of `coeffs` (uint8 [B,35], reference basis order).
 
     Returns (heights int8[B], iterations int8[B]) with 0 encoding infinity.  `devices` is a list of
     CUDA device indices (default: [0]); the batch is cut into contiguous blocks, one per device,
     each driven from its own host thread through its own context, and the results are gathered on
     the host -- surfaces are independent, there is no collective.
+
+    method: "matrix" (default; builds and streams the operator matrix like the reference's height_matrix) or
+    "naive" (the polynomial iteration without the matrix, qfs_heights_free: the on-device counterpart of the
+    reference's height_naive cross-check; same heights and iteration counts).
     """
+    if method not in ("matrix", "naive"):
+        raise DomainError(f"unknown method {method!r}, expected 'matrix' or 'naive'")
+    free = method == "naive"
     from .engine import get_engine
     c = _check_batch(p, coeffs, bound)
     B = c.shape[0]
@@ -173,14 +180,14 @@ def height_batch(p: int, coeffs, bound: int = 10, devices=None):
         return heights, iters
     blocks = split_blocks(B, len(devs))
     if len(blocks) == 1:
-        get_engine(p, devs[0]).heights(c, int(bound), out=(heights, iters))
+        get_engine(p, devs[0]).heights(c, int(bound), out=(heights, iters), matrix_free=free)
         return heights, iters
     errors = []
 
     def work(dev, start, cnt):
         try:
             get_engine(p, dev).heights(c[start:start + cnt], int(bound),
-                                       out=(heights[start:start + cnt], iters[start:start + cnt]))
+                                       out=(heights[start:start + cnt], iters[start:start + cnt]), matrix_free=free)
         except Exception as exc:  # re-raised on the caller's thread
             errors.append(exc)
 
@@ -194,12 +201,12 @@ def height_batch(p: int, coeffs, bound: int = 10, devices=None):
     return heights, iters
 
 
-def height_of_coeffs(p: int, coeffs, bound: int = 10, device: int = 0) -> HeightResult:
+def height_of_coeffs(p: int, coeffs, bound: int = 10, device: int = 0, method: str = "matrix") -> HeightResult:
     """HeightResult of one quartic given as its 35-entry coefficient vector."""
     c = np.asarray(coeffs)
     if c.shape != (NCOEFF,):
         raise DomainError(f"expected a {NCOEFF}-entry coefficient vector, got shape {c.shape}")
-    hs, its = height_batch(p, c.reshape(1, NCOEFF), bound, devices=[device])
+    hs, its = height_batch(p, c.reshape(1, NCOEFF), bound, devices=[device], method=method)
     return HeightResult(decode_height(hs[0]), int(bound), int(its[0]))
 
 
@@ -215,3 +222,14 @@ def height_matrix(prob, algorithm: str = "wics", device: int = 0) -> HeightResul
     _check_engine_shape(prob.p, prob.n)
     c = coeff_vector(prob.f, prob.p)
     return height_of_coeffs(prob.p, c, prob.bound, device)
+
+
+def height_naive(prob, device: int = 0) -> HeightResult:
+    """Height by the polynomial iteration g <- u(Delta g) without the operator matrix (height.py:97-116), on the GPU.
+
+    The reference keeps this driver as the independent check of height_matrix (same height, bound_used and
+    iterations: tests/test_acceptance.py:128-138); here it is the matrix-free kernel of csrc/qfs_free.cuh.
+    """
+    _check_engine_shape(prob.p, prob.n)
+    c = coeff_vector(prob.f, prob.p)
+    return height_of_coeffs(prob.p, c, prob.bound, device, method="naive")

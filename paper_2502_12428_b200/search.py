@@ -399,14 +399,12 @@ def verify_fixtures(text: str, n: int = 4, primes=None, jobs: int = 1, method: s
                     compute=None):
     """Recompute each fixture row's height on the GPU; verdicts in file order (search.py:219-229).
 
-    Rows are grouped by prime and each group is one batched call.  `method` is accepted for signature
-    compatibility; "naive" (the reference's polynomial iteration) has no GPU path and is rejected.
+    Rows are grouped by prime and each group is one batched call.  `method` = "matrix" or "naive" as in the
+    reference ("naive" = the matrix-free polynomial iteration, csrc/qfs_free.cuh).
     `jobs` is ignored (one batched call replaces the reference's process pool).
     """
     if method not in ("matrix", "naive"):
         raise DomainError(f"unknown method {method!r}")
-    if method == "naive":
-        raise DomainError("method='naive' is the reference's CPU cross-check; the GPU engine implements 'matrix'")
     rows = parse_fixtures(text, n)
     if primes is not None:
         keep = set(primes)
@@ -418,7 +416,7 @@ def verify_fixtures(text: str, n: int = 4, primes=None, jobs: int = 1, method: s
         for i in idx:
             SurfaceProblem(p, n, rows[i].f)  # the reference validates every row the same way
         if compute is None:
-            codes, _ = height_batch(p, coeffs, default_bound(n), devices=devices)
+            codes, _ = height_batch(p, coeffs, default_bound(n), devices=devices, method=method)
         else:
             codes, _ = compute(p, coeffs, default_bound(n), 0)
         for i, c in zip(idx, codes):

@@ -125,14 +125,12 @@ def test_cli_exit_codes_before_any_compute(capsys, tmp_path):
     assert rc == 3
     rc, _, err = run(capsys, "height", "--p", "5", "--poly", "x1^4+x2^4", "--nvars", "4", "--bound", "0")
     assert rc == 3 and "bound" in err
-    rc, _, err = run(capsys, "height", "--p", "5", "--poly", "x1^4+x2^4+x3^4+x4^4", "--method", "naive")
-    assert rc == 3 and "naive" in err
     rc, _, err = run(capsys, "search", "--p", "5", "--count", "0")
     assert rc == 3
     rc, _, err = run(capsys, "matrix", "--p", "4", "--poly", "x1^4+x2^4+x3^4+x4^4", "--out", str(tmp_path / "m"))
     assert rc == 3
-    rc, _, err = run(capsys, "verify", "--method", "naive")
-    assert rc == 3
+    with pytest.raises(SystemExit):
+        run(capsys, "verify", "--method", "bogus")
 
 
 def test_cli_reports_a_missing_engine_instead_of_falling_back(capsys):

@@ -182,3 +182,31 @@ def test_results_do_not_depend_on_what_the_workspaces_held(p):
     if rows:
         assert [int(h) for h in want_h[:len(rows)]] == [0 if r["height"] in ("inf", None) or r["height"] == 0 else int(r["height"]) for r in rows] \
             or True  # heights of the published rows are pinned in test_verify_fixtures_on_gpu
+
+
+def test_matrix_free_iteration_equals_the_reference_heights():
+    """qfs_heights_free (polynomial iteration, no Delta, no M) against the heights AND iteration counts the
+    reference produced for its seeded streams (10000 F_5, 2000 F_7, 3000 F_3), and against the matrix path."""
+    import paper_2502_12428_b200 as q
+    for p, name in ((3, "heights_p3_seed0_w0_3000.npz"), (5, "heights_p5_seed0_w0_10000.npz"), (7, "heights_p7_seed0_w0_2000.npz")):
+        z = np.load(os.path.join(GOLDEN, name))
+        hs, its = q.height_batch(p, z["coeffs"], 10, method="naive")
+        assert np.array_equal(hs.astype(np.int64), z["heights"].astype(np.int64))
+        assert np.array_equal(its.astype(np.int64), z["iters"].astype(np.int64))
+        hm, im = q.height_batch(p, z["coeffs"], 10)
+        assert np.array_equal(hs, hm) and np.array_equal(its, im)
+
+
+def test_matrix_free_bounds_fixtures_and_drivers():
+    import paper_2502_12428_b200 as q
+    verdicts = q.verify_fixtures(open(q.fixtures_path()).read(), method="naive")
+    assert len(verdicts) == 32 and all(v.ok for v in verdicts)
+    dwork5 = q.SurfaceProblem(5, 4, q.parse_poly("x1^4+x2^4+x3^4+x4^4+x1*x2*x3*x4", 4, 5))
+    assert q.height_naive(dwork5) == q.height_matrix(dwork5) == q.HeightResult(math.inf, 10, 9)
+    for bound in (1, 2, 3, 4, 7):
+        prob = q.SurfaceProblem(5, 4, dwork5.f, bound)
+        assert q.height_naive(prob) == q.height_matrix(prob) == q.HeightResult(math.inf, bound, bound - 1)
+    c = q.sample_block(11, 300, 5, 0)
+    h0, i0 = q.height_batch(11, c)
+    h1, i1 = q.height_batch(11, c, method="naive")
+    assert np.array_equal(h0, h1) and np.array_equal(i0, i1)

@@ -82,6 +82,16 @@ def test_cli_matrix_verify_bench(capsys, tmp_path):
     assert rc == 3 and "not supported" in err
     rc, out, _ = run(capsys, "height", "--p", "5", "--poly", fermat)
     assert rc == 0 and "height 1" in out and "iterations 0" in out
+    # the two methods agree, as in the reference's tests/test_cli.py:32-40
+    results = {}
+    for method in ("naive", "matrix"):
+        rc, out, _ = run(capsys, "height", "--p", "5", "--poly", fermat + "+x1*x2*x3*x4", "--method", method, "--json")
+        assert rc == 0
+        results[method] = json.loads(out)
+    assert results["naive"]["height"] == results["matrix"]["height"] == "inf"
+    assert results["naive"]["iterations"] == results["matrix"]["iterations"] == 9
+    rc, out, _ = run(capsys, "verify", "--method", "naive", "--primes", "5,7")
+    assert rc == 0 and "22 rows, 0 mismatches" in out
     for what in ("power", "mts", "matvec", "height"):
         rc, out, _ = run(capsys, "bench", "--p", "5", "--what", what, "--reps", "1")
         assert rc == 0 and "mean=" in out

@@ -174,7 +174,7 @@ def test_verify_fixtures_and_spectrum():
     with pytest.raises(q.ParseError):
         q.parse_fixtures("5 ; 2")
     with pytest.raises(q.DomainError):
-        q.verify_fixtures(text, primes=[5], method="naive")
+        q.verify_fixtures(text, primes=[5], method="bogus")
     wit, hist, blocks = q.spectrum_search(3, block=400, rng_seed=0, bound=10, max_blocks=3, compute=cpu_compute, want=[1, 2, 3])
     assert {1, 2, 3} <= set(wit) and blocks == 1 and hist.total == 400
     for line, h in zip(q.spectrum_rows(wit).splitlines(), sorted(wit, key=lambda x: (x == 0, x))):

@@ -14,13 +14,14 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--p", type=int, nargs="+", default=[5, 7])
 ap.add_argument("--batch", type=int, default=100000)
 ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--free", action="store_true", help="matrix-free mode (qfs_heights_free)")
 a = ap.parse_args()
 for p in a.p:
     c = bench.cached_block(p, a.batch, 0, 0)
     eng = get_engine(p, 0)
     acc = {}
     for i in range(3 + a.reps):
-        hs, its = eng.heights(c, 10)
+        hs, its = eng.heights(c, 10, matrix_free=a.free)
         if i >= 3:
             for k, v in eng.stats().items():
                 if k.startswith("ms_"):
