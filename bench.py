@@ -264,6 +264,41 @@ def measure_gpu(p, batch, steps, warmup, seed, rank, world, device, dist):
             "heights": heights, "iters": iters, "coeffs": host, "clocks": clocks}
 
 
+def measure_matrix_free(device, seed, checked):
+    """surfaces/s of qfs_heights_free on resident inputs (CUDA events), F_5 ... F_13, 100000 seeded quartics each;
+    for the primes in `checked` the heights and iteration counts are compared with the matrix path's."""
+    import torch
+    from paper_2502_12428_b200.engine import get_engine
+    out = {"note": "polynomial iteration g <- -f^(p-2) u(Delta_1(f) g) without Delta and without the operator matrix "
+                   "(csrc/qfs_free.cuh); same heights and iterations; not the path the roofline is quoted on"}
+    for p in (5, 7, 11, 13):
+        batch = 100000
+        host = cached_block(p, batch, seed, 0)
+        dev = torch.from_numpy(host).to(f"cuda:{device}")
+        hs = torch.empty(batch, dtype=torch.int8, device=dev.device)
+        its = torch.empty(batch, dtype=torch.int8, device=dev.device)
+        eng = get_engine(p, device)
+        for _ in range(3):
+            eng.heights(dev, 10, out=(hs, its), matrix_free=True)
+        torch.cuda.synchronize(device)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        steps = 5
+        e0.record()
+        for _ in range(steps):
+            eng.heights(dev, 10, out=(hs, its), matrix_free=True)
+        e1.record()
+        torch.cuda.synchronize(device)
+        ms = e0.elapsed_time(e1) / steps
+        h = hs.cpu().numpy()
+        entry = {"value": batch / (ms * 1e-3), "unit": "surfaces/s", "ms_per_step": ms, "batch": batch,
+                 "hard_per_s": float((h != 1).sum()) / (ms * 1e-3)}
+        if p in checked:
+            entry["equals_matrix_path"] = bool(np.array_equal(h, checked[p]["heights"]) and
+                                               np.array_equal(its.cpu().numpy(), checked[p]["iters"]))
+        out[f"F_{p}"] = entry
+    return out
+
+
 def gpu_line(args, p, res, world, with_cpu):
     batch, steps = args.batch, res["steps"]
     peak, peak_src = measured_peaks()
@@ -380,6 +415,10 @@ def main():
             l11 = gpu_line(args, 11, res11, world, with_cpu=False)
             line["also"]["F_11"] = {k: l11[k] for k in keep if k in l11}
         args.batch = saved
+        # The matrix-free iteration (qfs_heights_free): same heights and iteration counts, no Delta, no M.  NOT the contract
+        # path (the north star requires the operator matrix in HBM and the streamed matvec chain): reported beside it.
+        if rank == 0 and world == 1:
+            line["also"]["matrix_free"] = measure_matrix_free(local, args.seed, {5: res, 7: res7})
     if rank == 0:
         print(json.dumps(line))
     if dist is not None:
