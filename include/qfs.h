@@ -143,6 +143,18 @@ int qfs_stage_matrix(qfs_ctx *ctx, const uint8_t *delta, size_t B, uint8_t *M);
 int qfs_stage_matvec_chain(qfs_ctx *ctx, const uint8_t *M, const uint8_t *v0, size_t B, int max_steps,
                            uint8_t *trace, int8_t *heights, int8_t *iters);
 
+/* ---- plane cubic curves (n = 3) -------------------------------------------
+ * Heights of B cubic forms in x1..x3 over F_p (elliptic curves: height 1 =
+ * ordinary, 2 = supersingular), the other Calabi-Yau shape the reference's
+ * drivers are exercised on (height.py:63-144, tests/test_height.py:131-140).
+ * coeffs[B][10] over basis(3,3) in lex-ascending order, x1 most significant
+ * (index 0 = x3^3 ... 9 = x1^3); p an odd prime <= 53; bound >= 1 must be
+ * given (the reference has no default bound for n != 4, height.py:31-39).
+ * Context-free (one kernel, everything in shared memory); errors are reported
+ * through qfs_last_error(NULL).  Same output conventions as qfs_heights. */
+int qfs_cubic_heights(int device, int p, const uint8_t *coeffs, size_t B, int bound,
+                      int8_t *heights, int8_t *iters);
+
 /* ---- export ---------------------------------------------------------------
  * Operator matrices of B quartics (given by their coefficient vectors) in the
  * reference's export layout: M16[B][N][N] row-major uint16 little-endian --

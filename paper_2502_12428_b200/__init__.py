@@ -5,6 +5,7 @@ path this package replaces; heights come from hand-written sm_100a kernels behin
 (include/qfs.h).  There is no CPU fallback: without the library or a GPU the compute entry points
 raise EngineUnavailableError.
 """
+from .cubic import Cubic, cubic_height_batch
 from .errors import DomainError, EngineUnavailableError, InternalInvariantError, ParseError, QfsplitError
 from .height import (INFINITE, HeightResult, SurfaceProblem, default_bound, height_batch, height_matrix,
                      height_naive, height_of_coeffs, is_prime)
@@ -31,6 +32,6 @@ __all__ = [
     "FixtureRow", "FixtureVerdict", "FoundSurface", "HeightHistogram", "SearchConfig", "found_surfaces_text",
     "histogram_text", "parse_fixtures", "run_search", "sample_block", "sample_surface", "spectrum_rows",
     "spectrum_search", "verify_fixtures", "fixtures_path",
-    "MtsMatrix", "build_mts", "build_mts_batch", "matrix_from_bytes", "matrix_from_text", "matrix_to_bytes",
+    "Cubic", "cubic_height_batch", "MtsMatrix", "build_mts", "build_mts_batch", "matrix_from_bytes", "matrix_from_text", "matrix_to_bytes",
     "matrix_to_text", "target_degree",
 ]

@@ -13,6 +13,7 @@
 
 #include "../../include/qfs.h"
 #include "qfs_chain.cuh"
+#include "qfs_cubic.cuh"
 #include "qfs_delta.cuh"
 #include "qfs_delta_direct.cuh"
 #include "qfs_free.cuh"
@@ -874,6 +875,58 @@ int qfs_stage_matrix(qfs_ctx* ctx, const uint8_t* delta, size_t B, uint8_t* M)
     if (!ctx) return QFS_EINVAL;
     if (B && (!delta || !M)) return fail(ctx, QFS_EINVAL, "NULL buffer");
     QFS_FOR_PRIME(ctx->p, run_stage_matrix, ctx, delta, B, M)
+}
+
+int qfs_cubic_heights(int device, int p, const uint8_t* coeffs, size_t B, int bound, int8_t* heights, int8_t* iters)
+{
+    qfs_ctx* ctx = nullptr;  // errors of this context-free entry go where qfs_create's go: qfs_last_error(NULL)
+    if (p < 3 || p > QFS_CUBIC_MAXP || p % 2 == 0) return fail(ctx, QFS_EINVAL, "cubic curves: p=%d is not an odd prime <= %d", p, QFS_CUBIC_MAXP);
+    for (int q = 3; q * q <= p; q += 2)
+        if (p % q == 0) return fail(ctx, QFS_EINVAL, "p=%d is not prime", p);
+    if (bound < 1 || bound > 127) return fail(ctx, QFS_EINVAL, "bound must be in 1..127, got %d", bound);
+    if (B == 0) return QFS_OK;
+    if (!coeffs || !heights || !iters) return fail(ctx, QFS_EINVAL, "NULL buffer");
+    if (B > 0x7fffffffULL) return fail(ctx, QFS_EINVAL, "batch too large");
+    CU(cudaSetDevice(device));
+    const bool in_dev = is_device_ptr(coeffs), h_dev = is_device_ptr(heights), i_dev = is_device_ptr(iters);
+    uint8_t* d_c = nullptr;
+    int8_t *d_h = nullptr, *d_i = nullptr;
+    int* d_err = nullptr;
+    int rc = QFS_OK, h_err = 0;
+    auto cleanup = [&]() {
+        if (!in_dev && d_c) cudaFree(d_c);
+        if (!h_dev && d_h) cudaFree(d_h);
+        if (!i_dev && d_i) cudaFree(d_i);
+        if (d_err) cudaFree(d_err);
+    };
+#define CUC(call)                                                                                          \
+    do {                                                                                                   \
+        cudaError_t e_ = (call);                                                                           \
+        if (e_ != cudaSuccess) {                                                                           \
+            rc = fail(ctx, e_ == cudaErrorMemoryAllocation ? QFS_ENOMEM : QFS_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+            cleanup();                                                                                     \
+            return rc;                                                                                     \
+        }                                                                                                  \
+    } while (0)
+    if (in_dev) d_c = const_cast<uint8_t*>(coeffs);
+    else { CUC(cudaMalloc(&d_c, B * 10)); CUC(cudaMemcpy(d_c, coeffs, B * 10, cudaMemcpyHostToDevice)); }
+    if (h_dev) d_h = heights; else CUC(cudaMalloc(&d_h, B));
+    if (i_dev) d_i = iters; else CUC(cudaMalloc(&d_i, B));
+    CUC(cudaMalloc(&d_err, sizeof(int)));
+    CUC(cudaMemset(d_err, 0, sizeof(int)));
+    const size_t smem = qfs_cubic_smem(p);
+    CUC(cudaFuncSetAttribute(k_cubic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_cubic<<<(unsigned)B, QFS_CUBIC_NT, smem>>>(d_c, (int)B, p, bound - 1, d_h, d_i, d_err);
+    CUC(cudaGetLastError());
+    CUC(cudaMemcpy(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost));
+    if (!h_dev) CUC(cudaMemcpy(heights, d_h, B, cudaMemcpyDeviceToHost));
+    if (!i_dev) CUC(cudaMemcpy(iters, d_i, B, cudaMemcpyDeviceToHost));
+    CUC(cudaDeviceSynchronize());
+#undef CUC
+    cleanup();
+    if (h_err & QFS_ERRBIT_INPUT) return fail(ctx, QFS_EINVAL, "input violates a precondition: a coefficient >= p or the zero form");
+    if (h_err & QFS_ERRBIT_INVARIANT) return fail(ctx, QFS_EINVARIANT, "Witt-carry numerator not divisible by p");
+    return QFS_OK;
 }
 
 int qfs_debug_fill_workspaces(qfs_ctx* ctx, int byte)

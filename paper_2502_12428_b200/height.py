@@ -116,7 +116,7 @@ def decode_height(h: int):
 
 def _check_engine_shape(p: int, n: int = NVARS):
     if n != NVARS:
-        raise DomainError(f"the GPU engine computes heights of quartics in 4 variables; got n={n}")
+        raise DomainError(f"the GPU engine computes heights of quartics in 4 variables and of cubics in 3; got n={n}")
     if p not in SUPPORTED_PRIMES:
         raise DomainError(f"p={p} is not supported by the GPU engine (supported: {SUPPORTED_PRIMES})")
 
@@ -219,6 +219,8 @@ def height_matrix(prob, algorithm: str = "wics", device: int = 0) -> HeightResul
     """
     if algorithm not in ("triv", "merge", "wics"):
         raise DomainError(f"unknown matrix algorithm {algorithm!r}")
+    if prob.n == 3:
+        return _cubic_height(prob, device)
     _check_engine_shape(prob.p, prob.n)
     c = coeff_vector(prob.f, prob.p)
     return height_of_coeffs(prob.p, c, prob.bound, device)
@@ -230,6 +232,16 @@ def height_naive(prob, device: int = 0) -> HeightResult:
     The reference keeps this driver as the independent check of height_matrix (same height, bound_used and
     iterations: tests/test_acceptance.py:128-138); here it is the matrix-free kernel of csrc/qfs_free.cuh.
     """
+    if prob.n == 3:
+        return _cubic_height(prob, device)
     _check_engine_shape(prob.p, prob.n)
     c = coeff_vector(prob.f, prob.p)
     return height_of_coeffs(prob.p, c, prob.bound, device, method="naive")
+
+
+def _cubic_height(prob, device: int = 0) -> HeightResult:
+    """n = 3 (plane cubic curves): one kernel, csrc/qfs_cubic.cuh.  The operator matrices are at most 703 x 703 here, so
+    both drivers run the matrix-free iteration; the results are the reference's (tests/golden/cubics.json)."""
+    from .cubic import cubic_height_batch, cubic_vector
+    hs, its = cubic_height_batch(prob.p, cubic_vector(prob.f, prob.p)[None, :], prob.bound, device)
+    return HeightResult(decode_height(hs[0]), int(prob.bound), int(its[0]))

@@ -187,7 +187,7 @@ def _parse_text_terms(text: str):
         terms.append((tuple(exps), coeff))
 
 
-def _parse_compact_terms(text: str):
+def _parse_compact_terms(text: str, nvars: int = NVARS):
     out = []
     pos = 0
     for chunk in text.splitlines():
@@ -207,8 +207,8 @@ def _parse_compact_terms(text: str):
                 raise ParseError(f"malformed term {line!r}", start) from None
             if coeff < 0 or any(e < 0 for e in exps):
                 raise ParseError(f"negative value in {line!r}", start)
-            if len(exps) != NVARS:
-                raise ParseError(f"term has {len(exps)} exponents, expected {NVARS}", start)
+            if len(exps) != nvars:
+                raise ParseError(f"term has {len(exps)} exponents, expected {nvars}", start)
             out.append((exps, coeff))
     if not out:
         raise ParseError("no terms found", 0)
@@ -217,10 +217,29 @@ def _parse_compact_terms(text: str):
 
 def parse_poly(text: str, nvars: int | None = NVARS, modulus: int | None = None) -> Quartic:
     """Parse either text format (auto-detected by ':') into a Quartic over F_modulus."""
-    if nvars not in (None, NVARS):
-        raise DomainError(f"the GPU engine handles quartics in {NVARS} variables, got nvars={nvars}")
+    if nvars not in (None, NVARS, 3):
+        raise DomainError(f"the GPU engine handles quartics in {NVARS} variables and cubics in 3, got nvars={nvars}")
     if modulus is None:
         raise DomainError("parse_poly needs the modulus p")
+    if nvars is None and ":" not in text:
+        # the reference infers the variable count from the highest variable that appears (polyring.py:438-520)
+        used = max((max((j + 1 for j, e in enumerate(exps) if e), default=0) for exps, _ in _parse_text_terms(text)), default=0)
+        if used == 3:
+            nvars = 3
+        elif used < 3:
+            raise DomainError(f"f has {used} variables; pass nvars (the GPU engine handles quartics in 4 variables and "
+                              f"cubics in 3), and f must be homogeneous of degree nvars (Calabi-Yau condition)")
+    if nvars == 3:
+        from .cubic import Cubic
+        if ":" in text:
+            terms = _parse_compact_terms(text, 3)
+        else:
+            terms = []
+            for exps, c in _parse_text_terms(text):  # the term scanner works with four exponent slots
+                if exps[3]:
+                    raise ParseError("variable x4 exceeds nvars=3", 0)
+                terms.append((tuple(exps[:3]), c))
+        return Cubic.from_terms(terms, modulus)
     terms = _parse_compact_terms(text) if ":" in text else _parse_text_terms(text)
     return Quartic.from_terms(terms, modulus)
 
