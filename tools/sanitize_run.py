@@ -21,4 +21,12 @@ for p in primes:
     hs, its = eng.heights(c, 10)
     d = eng.stage_delta(c[:3])
     m = eng.export_matrix(c[:2])
+    hf, itf = eng.heights(c, 10, matrix_free=True)
+    assert np.array_equal(hs, hf) and np.array_equal(its, itf)
     print(p, np.bincount(hs.astype(np.int64)).tolist(), d.shape, m.shape, flush=True)
+rng = np.random.default_rng(5)
+for p in (3, 5, 13):
+    hs, its = q.cubic_height_batch(p, rng.integers(1, p, size=(40, 10)).astype(np.uint8), 5)
+    print("cubic", p, np.bincount(hs.astype(np.int64)).tolist(), flush=True)
+if os.environ.get("QFS_DELTA_DIRECT"):
+    print("k_delta_direct was used for Delta")
