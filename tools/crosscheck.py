@@ -1,0 +1,44 @@
+#!/usr/bin/env python3
+"""Large-scale cross-check on the GPU: the matrix path (qfs_heights: Delta, operator matrix in HBM, streamed matvec chain)
+against the matrix-free polynomial iteration (qfs_heights_free) on seeded random quartics -- two different algorithms that
+must agree on every height and every iteration count.
+
+    python tools/crosscheck.py --p 5 --count 10000000 [--block 1000000] [--seed 1]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2502_12428_b200 as q  # noqa: E402
+from paper_2502_12428_b200.engine import get_engine  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--p", type=int, default=5)
+ap.add_argument("--count", type=int, default=10000000)
+ap.add_argument("--block", type=int, default=1000000)
+ap.add_argument("--seed", type=int, default=1)
+a = ap.parse_args()
+eng = get_engine(a.p, 0)
+hist = np.zeros(12, dtype=np.int64)
+mism = 0
+t_m = t_f = 0.0
+done = 0
+w = 0
+while done < a.count:
+    n = min(a.block, a.count - done)
+    c = q.sample_block(a.p, n, a.seed, w)
+    t0 = time.perf_counter(); hm, im = eng.heights(c, 10); t1 = time.perf_counter()
+    hf, jf = eng.heights(c, 10, matrix_free=True); t2 = time.perf_counter()
+    t_m += t1 - t0; t_f += t2 - t1
+    mism += int((hm != hf).sum() + (im != jf).sum())
+    hist += np.bincount(hm.astype(np.int64), minlength=12)[:12]
+    done += n; w += 1
+print(json.dumps({"p": a.p, "surfaces": done, "seed": a.seed, "mismatches": mism,
+                  "histogram": {("inf" if h == 0 else str(h)): int(v) for h, v in enumerate(hist) if v},
+                  "matrix_path_s": round(t_m, 2), "matrix_free_s": round(t_f, 2)}))
+sys.exit(1 if mism else 0)
