@@ -97,66 +97,64 @@ def build_mts_batch(p: int, coeffs, device: int = 0) -> np.ndarray:
     return get_engine(p, device).export_matrix(_check_batch(p, coeffs, 10))
 
 
+_HEADER = struct.Struct("<6I")  # rows, cols, p, n, d, d'
+
+
 def matrix_to_text(m: MtsMatrix) -> str:
-    """Header line "rows cols p", then one text row per matrix row (mtsmatrix.py:301-306)."""
-    lines = [f"{m.rows} {m.cols} {m.p}"]
-    digits = np.char.mod("%d", m.entries)
-    lines.extend(" ".join(row) for row in digits)
-    return "\n".join(lines) + "\n"
+    """The text export: a "rows cols p" line, then the entries row by row, blank-separated (mtsmatrix.py:301-306)."""
+    body = "\n".join(" ".join(row) for row in np.char.mod("%d", m.entries))
+    return f"{m.rows} {m.cols} {m.p}\n{body}\n"
 
 
-def _degree_for_size(size: int, n: int, what: str) -> int:
-    if n < 2:
+def _basis_degree(count: int, nvars: int, what: str) -> int:
+    """The degree whose monomial basis in `nvars` variables has `count` elements (the text header does not store it)."""
+    if nvars < 2:
         raise DomainError("degree inference needs at least 2 variables")
-    deg = 0
-    while True:
-        count = math.comb(deg + n - 1, n - 1)
-        if count == size:
-            return deg
-        if count > size:
-            raise DomainError(f"no degree-{n} basis has {size} {what}")
-        deg += 1
+    degree, size = 0, 1
+    while size < count:
+        degree += 1
+        size = size * (degree + nvars - 1) // degree      # C(degree+n-1, n-1) from C(degree+n-2, n-1)
+    if size != count:
+        raise DomainError(f"no degree-{nvars} basis has {count} {what}")
+    return degree
 
 
 def matrix_from_text(text: str, n: int, d=None, dprime=None) -> MtsMatrix:
-    """Inverse of matrix_to_text (mtsmatrix.py:322-347); n comes from the caller, degrees are inferred unless given."""
+    """Read the text export back (mtsmatrix.py:322-347).  `n` comes from the caller; degrees are inferred unless given."""
     lines = [ln for ln in text.splitlines() if ln.strip()]
     if not lines:
         raise DomainError("empty matrix text")
     head = lines[0].split()
     if len(head) != 3:
         raise DomainError(f"matrix header needs 'rows cols p', got {lines[0]!r}")
-    rows, cols, p = (int(v) for v in head)
+    rows, cols, p = map(int, head)
     if len(lines) - 1 != rows:
         raise DomainError(f"expected {rows} entry rows, got {len(lines) - 1}")
-    if d is None:
-        d = _degree_for_size(cols, n, "columns")
-    if dprime is None:
-        dprime = _degree_for_size(rows, n, "rows")
-    entries = np.zeros((rows, cols), dtype=np.uint16)
-    for i, line in enumerate(lines[1:]):
-        vals = line.split()
-        if len(vals) != cols:
-            raise DomainError(f"row {i} has {len(vals)} entries, expected {cols}")
-        entries[i] = [int(v) for v in vals]
-    return MtsMatrix(entries, n, d, dprime, p)
+    widths = [len(ln.split()) for ln in lines[1:]]
+    for i, w in enumerate(widths):
+        if w != cols:
+            raise DomainError(f"row {i} has {w} entries, expected {cols}")
+    entries = np.array(" ".join(lines[1:]).split(), dtype=np.int64).reshape(rows, cols)
+    return MtsMatrix(entries, n,
+                     _basis_degree(cols, n, "columns") if d is None else d,
+                     _basis_degree(rows, n, "rows") if dprime is None else dprime, p)
 
 
 def matrix_to_bytes(m: MtsMatrix) -> bytes:
-    """Magic, six uint32 header words (rows, cols, p, n, d, d'), uint16 entries, little-endian (mtsmatrix.py:350-365)."""
-    head = struct.pack("<6I", m.rows, m.cols, m.p, m.nvars, m.source_degree, m.target_degree)
-    return _MAGIC + head + m.entries.astype("<u2").tobytes()
+    """The binary export: "QFSMTX01", six little-endian uint32 (rows, cols, p, n, d, d'), then the entries as
+    little-endian uint16 in row-major order (mtsmatrix.py:350-365)."""
+    return b"".join((_MAGIC, _HEADER.pack(m.rows, m.cols, m.p, m.nvars, m.source_degree, m.target_degree),
+                     m.entries.astype("<u2", copy=False).tobytes()))
 
 
 def matrix_from_bytes(data: bytes) -> MtsMatrix:
-    """Inverse of matrix_to_bytes (mtsmatrix.py:368-380)."""
-    if len(data) < len(_MAGIC) + 24:
+    """Read the binary export back (mtsmatrix.py:368-380)."""
+    start = len(_MAGIC) + _HEADER.size
+    if len(data) < start:
         raise DomainError("binary matrix data is truncated")
-    if data[: len(_MAGIC)] != _MAGIC:
+    if not data.startswith(_MAGIC):
         raise DomainError("bad magic; not a matrix export")
-    rows, cols, p, n, d, dprime = struct.unpack_from("<6I", data, len(_MAGIC))
-    body = data[len(_MAGIC) + 24:]
-    if len(body) != 2 * rows * cols:
-        raise DomainError(f"entry block holds {len(body)} bytes, expected {2 * rows * cols}")
-    entries = np.frombuffer(body, dtype="<u2").astype(np.uint16).reshape(rows, cols)
-    return MtsMatrix(entries, n, d, dprime, p)
+    rows, cols, p, n, d, dprime = _HEADER.unpack_from(data, len(_MAGIC))
+    if len(data) - start != 2 * rows * cols:
+        raise DomainError(f"entry block holds {len(data) - start} bytes, expected {2 * rows * cols}")
+    return MtsMatrix(np.frombuffer(data, dtype="<u2", offset=start).reshape(rows, cols), n, d, dprime, p)
