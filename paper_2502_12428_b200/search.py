@@ -240,7 +240,7 @@ def run_search(cfg: SearchConfig, devices=None, compute=None):
 # ---- spectrum search (paper section 7) --------------------------------------------------------
 
 def spectrum_search(p: int, block: int = 100000, rng_seed: int = 0, bound: int = 10, max_blocks: int = 1000,
-                    devices=None, compute=None, want=None, progress=None):
+                    devices=None, compute=None, want=None, progress=None, method: str = "matrix"):
     """Sample seeded blocks until every height in `want` (default 1..bound and infinity) has a witness.
 
     Block b uses the reference stream `default_rng([rng_seed, b])`, so any witness can be regenerated from
@@ -248,6 +248,7 @@ def spectrum_search(p: int, block: int = 100000, rng_seed: int = 0, bound: int =
     device) and retired in block order, so the result does not depend on the number of devices.
     Returns (witnesses {height code: (block, index, Quartic)}, HeightHistogram, blocks_done); height code
     0 = infinity.  `progress(blocks_done, hist, witnesses)` is called after every retired block.
+    `method` = "matrix" (operator matrix built and streamed) or "naive" (matrix-free iteration); same heights.
     """
     import queue
     devs = [0] if devices is None else [int(d) for d in devices]
@@ -297,7 +298,7 @@ def spectrum_search(p: int, block: int = 100000, rng_seed: int = 0, bound: int =
                 if stop.is_set():
                     continue
                 if compute is None:
-                    codes, _ = height_batch(p, coeffs, bound, devices=[dev])
+                    codes, _ = height_batch(p, coeffs, bound, devices=[dev], method=method)
                 else:
                     codes, _ = compute(p, coeffs, bound, dev)
                 with cond:

@@ -25,6 +25,9 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--devices", default="0")
     ap.add_argument("--verify", action="store_true")
+    ap.add_argument("--method", choices=("matrix", "naive"), default="matrix",
+                    help="matrix: operator matrix in HBM + matvec chain (contract path); naive: matrix-free iteration")
+    ap.add_argument("--want", default=None, help="comma-separated heights to look for (inf allowed); default 1..10,inf")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     devs = [int(x) for x in a.devices.split(",")]
@@ -34,12 +37,14 @@ def main():
         if n % 10 == 0:
             print(f"[{time.perf_counter() - t0:7.1f}s] blocks {n} samples {hist.total} seen {sorted(wit)}", file=sys.stderr, flush=True)
 
-    wit, hist, blocks = q.spectrum_search(a.p, a.block, a.seed, 10, a.max_blocks, devices=devs, progress=progress)
+    want = None if a.want is None else [float("inf") if t == "inf" else int(t) for t in a.want.split(",")]
+    wit, hist, blocks = q.spectrum_search(a.p, a.block, a.seed, 10, a.max_blocks, devices=devs, progress=progress,
+                                          method=a.method, want=want)
     dt = time.perf_counter() - t0
     rows = q.spectrum_rows(wit)
     print(rows)
-    summary = {"p": a.p, "seed": a.seed, "block": a.block, "blocks": blocks, "samples": hist.total, "seconds": dt,
-               "surfaces_per_s": hist.total / dt, "histogram": hist.as_dict(), "complete": set(range(11)) <= set(wit),
+    summary = {"p": a.p, "method": a.method, "seed": a.seed, "block": a.block, "blocks": blocks, "samples": hist.total, "seconds": dt,
+               "surfaces_per_s": hist.total / dt, "histogram": hist.as_dict(), "complete": (set(range(11)) if want is None else {0 if h == float("inf") else h for h in want}) <= set(wit),
                "witnesses": {("inf" if h == 0 else str(h)): {"block": b, "index": i} for h, (b, i, _) in sorted(wit.items())}}
     if a.verify:
         import oracle
