@@ -78,7 +78,6 @@ struct qfs_ctx {
     int staged_nbuf = 1;
     int staged_multi = 0;
     int delta_direct = 0;                           // QFS_DELTA_DIRECT: use k_delta_direct for every prime (cross-check)
-    int staged_nocopy = 0;                          // QFS_STAGED_NOCOPY: measurement aid (skips the staging copies; results are garbage)
     int matrix_version = 6;                         // 6 = shared-memory staged builder, 4 = direct gather (QFS_MATRIX_V)
     int* h_flags = nullptr;                         // pinned mirror of flags
 };
@@ -256,7 +255,6 @@ int build_tables(qfs_ctx* ctx)
         CU(cudaFuncSetAttribute(k_matrix_staged<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->staged_smem));
         CU(cudaFuncSetAttribute(k_matrix_staged<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->staged_smem));
         if (const char* e = getenv("QFS_MATRIX_V")) ctx->matrix_version = atoi(e);
-        ctx->staged_nocopy = getenv("QFS_STAGED_NOCOPY") ? 2 : 0;
     }
     CU(cudaFuncSetAttribute(k_fedder<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, PowerCfg<P>::FED_SMEM));
     CU(cudaFuncSetAttribute(k_power_full<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, PowerCfg<P>::FULL_SMEM));
@@ -358,7 +356,7 @@ int launch_matrix(qfs_ctx* ctx, int count, const uint8_t* v0, uint8_t* v1)
             }
             k_matrix_staged<P, true><<<sgrid, SC::NTL, ctx->staged_smem, ctx->stream>>>(
                 ctx->delta.as<uint8_t>(), ctx->colinfo.as<uint32_t>(), ctx->items.as<PanelItem>(), ctx->M.as<uint8_t>(), v0, v1,
-                ctx->vacc.as<int>(), count, ctx->staged_bufwords, ctx->staged_nbuf, ctx->staged_multi | ctx->staged_nocopy);
+                ctx->vacc.as<int>(), count, ctx->staged_bufwords, ctx->staged_nbuf, ctx->staged_multi);
             ctx->stats.kernel_launches++;
             CU(cudaGetLastError());
             if (ctx->staged_multi) {
@@ -369,7 +367,7 @@ int launch_matrix(qfs_ctx* ctx, int count, const uint8_t* v0, uint8_t* v1)
         } else {
             k_matrix_staged<P, false><<<sgrid, SC::NTL, ctx->staged_smem, ctx->stream>>>(
                 ctx->delta.as<uint8_t>(), ctx->colinfo.as<uint32_t>(), ctx->items.as<PanelItem>(), ctx->M.as<uint8_t>(), nullptr,
-                nullptr, nullptr, count, ctx->staged_bufwords, ctx->staged_nbuf, ctx->staged_multi | ctx->staged_nocopy);
+                nullptr, nullptr, count, ctx->staged_bufwords, ctx->staged_nbuf, ctx->staged_multi);
             ctx->stats.kernel_launches++;
             CU(cudaGetLastError());
         }

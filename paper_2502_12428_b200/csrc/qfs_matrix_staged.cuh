@@ -200,7 +200,6 @@ k_matrix_staged(const uint8_t* __restrict__ delta_all, const uint32_t* __restric
     const uint32_t sm_base = (uint32_t)__cvta_generic_to_shared(sm);
     const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(s_bar);
     const uint32_t bufbytes = 4u * (uint32_t)bufwords;
-    const bool nocopy = flags & 2;  // measurement aid: skip the staging copies (results are garbage)
 
     if (tid == 0) {
         int so = C::ZW, n = 0;
@@ -234,7 +233,7 @@ k_matrix_staged(const uint8_t* __restrict__ delta_all, const uint32_t* __restric
         const uint32_t vlo = (4u * C::V * it.glo) & ~15u;
         const uint32_t vlen = FUSE ? min((uint32_t)S::pitch, (4u * C::V * (it.glo + it.ngrp) + 15u) & ~15u) - vlo : 0u;
         auto issue = [&](int quad, int b) {
-            if (nocopy || (n == 0 && !FUSE)) return;
+            if (n == 0 && !FUSE) return;
             const uint32_t bar = bar0 + 8u * b;
             const uint8_t* dq = delta_all + (size_t)quad * S::quad_stride;
             if (lane == 0) mbar_expect_tx(bar, total + 4u * vlen);
@@ -291,7 +290,7 @@ k_matrix_staged(const uint8_t* __restrict__ delta_all, const uint32_t* __restric
         }
         sp[k] = sm_base + 4u * (uint32_t)(idx + P * team);  // row t = team
     }
-    const bool staged = (s_ncp > 0 || FUSE) && !nocopy;
+    const bool staged = s_ncp > 0 || FUSE;
     // this thread's words of v0 inside the staged window (buffer 0, surface 0)
     const uint32_t vaddr = sm_base + bufbytes - 4u * C::VWORDS + (4u * C::V * grp - ((4u * C::V * it.glo) & ~15u));
     // team rows t = team, team + TEAMS, ...: r3 = R - t
@@ -317,7 +316,7 @@ k_matrix_staged(const uint8_t* __restrict__ delta_all, const uint32_t* __restric
         for (int s = 0; s < 4; ++s)
 #pragma unroll
             for (int j = 0; j < C::V; ++j)
-                vw[j][s] = (FUSE && live && !nocopy) ? lds32(vaddr + b * bufbytes + s * C::VSEG + 4 * j) : 0u;
+                vw[j][s] = (FUSE && live) ? lds32(vaddr + b * bufbytes + s * C::VSEG + 4 * j) : 0u;
 
 #pragma unroll 1
         for (int blk = 0; blk < nblk; ++blk) {
