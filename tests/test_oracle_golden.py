@@ -118,3 +118,22 @@ def test_factorised_identities_match_reference_intermediates():
             I = tuple(5 * a + 4 - b for a, b in zip(tb[r], tb[c]))
             want = int(dl[mf.rank(80, I)]) if min(I) >= 0 else 0
             assert int(M[r, c]) == want
+
+
+@pytest.mark.parametrize("name", ["r1_spectrum_p5.txt", "r1_spectrum_p7.txt", "r1f_spectrum_p7_matrix_free.txt"])
+def test_spectrum_witnesses(name):
+    """The witnesses the GPU spectrum searches wrote (profiles/, fixture-table rows `p ; height ; poly`: one surface for
+    every height 1..10 and infinity over F_5 and F_7) recomputed by the CPU oracle."""
+    import paper_2502_12428_b200 as q
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    rows = [ln for ln in open(os.path.join(root, "profiles", name)) if ln.strip() and not ln.startswith("#")]
+    coeffs, want, p = [], [], None
+    for ln in rows:
+        p_s, h_s, poly = [t.strip() for t in ln.split(";", 2)]
+        p = int(p_s)
+        want.append(0 if h_s == "inf" else int(h_s))
+        coeffs.append(q.parse_poly(poly, 4, p).coeffs)
+    got, iters = oracle.heights_batch(np.stack(coeffs), p, 10)   # OpenMP over the surfaces
+    assert [int(h) for h in got] == want
+    assert [int(i) for i in iters] == [9 if h == 0 else h - 1 for h in want]
+    assert set(want) == set(range(11))
