@@ -204,11 +204,7 @@ def do_heights5():
 
 
 def do_heights7():
-    _heights(7, 2000)
-
-
-def do_heights7_10k():
-    """The F_7 counterpart of the north star's 10k-surface seeded set (about 40 minutes on 7 cores: ~11 s per hard surface)."""
+    """The F_7 counterpart of the north star's 10k-surface seeded set (38 minutes on 7 cores: ~11 s per hard surface)."""
     _heights(7, 10000)
 
 

@@ -103,7 +103,7 @@ def test_ragged_batches_and_chunking(p, B):
     coeffs = rng.integers(0, p, size=(B, 35)).astype(np.uint8)
     coeffs[(coeffs == 0).all(axis=1), 0] = 1
     # make sure the hard path is exercised: append known height>=2 rows of the golden stream
-    z = np.load(os.path.join(GOLDEN, f"heights_p{p}_seed0_w0_{ {3: 3000, 5: 10000, 7: 2000}[p] }.npz"))
+    z = np.load(os.path.join(GOLDEN, f"heights_p{p}_seed0_w0_{ {3: 3000, 5: 10000, 7: 10000}[p] }.npz"))
     hard = z["coeffs"][np.nonzero(z["heights"] != 1)[0][:B]]
     coeffs = np.concatenate([coeffs, hard]) if B else coeffs
     want = oracle.heights_batch(coeffs, p, 10) if len(coeffs) else (np.empty(0, np.int8),) * 2
@@ -186,9 +186,9 @@ def test_results_do_not_depend_on_what_the_workspaces_held(p):
 
 def test_matrix_free_iteration_equals_the_reference_heights():
     """qfs_heights_free (polynomial iteration, no Delta, no M) against the heights AND iteration counts the
-    reference produced for its seeded streams (10000 F_5, 2000 F_7, 3000 F_3), and against the matrix path."""
+    reference produced for its seeded streams (10000 F_5, 10000 F_7, 3000 F_3), and against the matrix path."""
     import paper_2502_12428_b200 as q
-    for p, name in ((3, "heights_p3_seed0_w0_3000.npz"), (5, "heights_p5_seed0_w0_10000.npz"), (7, "heights_p7_seed0_w0_2000.npz")):
+    for p, name in ((3, "heights_p3_seed0_w0_3000.npz"), (5, "heights_p5_seed0_w0_10000.npz"), (7, "heights_p7_seed0_w0_10000.npz")):
         z = np.load(os.path.join(GOLDEN, name))
         hs, its = q.height_batch(p, z["coeffs"], 10, method="naive")
         assert np.array_equal(hs.astype(np.int64), z["heights"].astype(np.int64))

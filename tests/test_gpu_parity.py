@@ -82,7 +82,7 @@ def test_stage_chain_golden(p):
 
 
 @pytest.mark.parametrize("p,name", [(3, "heights_p3_seed0_w0_3000"), (5, "heights_p5_seed0_w0_10000"),
-                                    (7, "heights_p7_seed0_w0_2000")])
+                                    (7, "heights_p7_seed0_w0_10000")])
 def test_heights_golden_sets(p, name):
     path = os.path.join(GOLDEN, name + ".npz")
     if not os.path.exists(path):

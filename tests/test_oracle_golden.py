@@ -62,7 +62,7 @@ def test_height_matrix_taps(p):
 
 
 @pytest.mark.parametrize("p,name,count", [(3, "heights_p3_seed0_w0_3000", 3000), (5, "heights_p5_seed0_w0_10000", 400),
-                                          (7, "heights_p7_seed0_w0_2000", 24)])
+                                          (7, "heights_p7_seed0_w0_10000", 300)])
 def test_seeded_streams(p, name, count):
     z = np.load(os.path.join(GOLDEN, name + ".npz"))
     hs, its = oracle.heights_batch(z["coeffs"][:count], p, 10)
