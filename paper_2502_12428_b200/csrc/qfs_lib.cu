@@ -224,7 +224,10 @@ int build_tables(qfs_ctx* ctx)
                 int lo = 0;
                 while (lo <= S::d) {
                     int dummy;
-                    auto fits = [&](int h) { return staged_of(lo, h) <= budget && groups_of(lo, h, dummy) <= SC::MAXG; };
+                    auto fits = [&](int h) {
+                        const int n = groups_of(lo, h, dummy);
+                        return staged_of(lo, h) <= budget && (n == 0 || dummy % SC::LINEG + n <= SC::MAXG);
+                    };
                     int hi = lo;
                     while (hi < S::d && fits(hi + 1)) ++hi;
                     if (hi >= last_start && hi < S::d) hi = last_start - 1;  // the tail blocks stay together

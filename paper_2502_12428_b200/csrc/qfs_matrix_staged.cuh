@@ -36,14 +36,24 @@ struct PanelItem {
 template <int P>
 struct StagedCfg {
     using S = Shape<P>;
-    static constexpr int V = (P >= 7) ? 2 : 1;                              // consecutive 32-bit words per thread (store width 4V bytes)
+#ifndef QFS_V5
+#define QFS_V5 1
+#endif
+    static constexpr int V = (P >= 7) ? 2 : (P == 5 ? QFS_V5 : 1);                              // consecutive 32-bit words per thread (store width 4V bytes)
     static constexpr int TEAMS = V;                          // row teams
-    static constexpr int NT = (P >= 13) ? 384 : (P == 7 ? 192 : (P >= 5 ? 256 : 64));  // consumer threads (p = 13: block c1 = 0 alone is 154 word groups; p = 7: 96-thread teams fit its ~91-group panels)
+#ifndef QFS_NT7
+#define QFS_NT7 192
+#endif
+    static constexpr int NT = (P >= 13) ? 384 : (P == 7 ? QFS_NT7 : (P >= 5 ? 256 : 64));  // consumer threads (p = 13: block c1 = 0 alone is 154 word groups; p = 7: 96-thread teams fit its ~91-group panels)
     static constexpr int TEAM = NT / TEAMS;                  // threads (= word groups) per team
     static constexpr int NTL = NT + 32;                      // launched: + the producer warp
     static constexpr int WORDS = S::pitch / 4;
     static constexpr int NGRP = WORDS / V;                   // word groups per row
     static constexpr int MAXG = TEAM;                        // most word groups a panel may own
+    // Rows that start on 128-byte lines (QFS_PITCH_ALIGN = 128): the warps of a team start at the line in front of the
+    // panel's first word group, so that every warp store covers whole lines (tools/micro/write_bw4.cu); the
+    // glo % LINEG threads in front of the panel repeat its first word group.
+    static constexpr int LINEG = (QFS_PITCH_ALIGN % 128 == 0) ? 128 / (4 * V) : 1;
     static constexpr int HEADRUNS = (V == 1) ? 2 : (V == 2 ? 4 : 5);  // runs covering the 4V-1 columns before a block
     static constexpr int MAXROWS = S::d + 1;
     static constexpr int SLICE = (P >= 11) ? 8 : (P >= 7 ? 8 : 16);        // quads per CTA
@@ -275,8 +285,9 @@ k_matrix_staged(const uint8_t* __restrict__ delta_all, const uint32_t* __restric
 
     // ---- consumers ----
     const int team = tid / C::TEAM, tt = tid - team * C::TEAM;
-    const int grp = it.glo + min(tt, (int)it.ngrp - 1);   // threads past the panel end repeat its last word group
-    const bool live = tt < (int)it.ngrp;
+    const int trel = tt - (int)(it.glo % C::LINEG);       // warps start on 128-byte lines of the row (LINEG > 1)
+    const int grp = it.glo + max(0, min(trel, (int)it.ngrp - 1));   // threads outside the panel repeat its first / last word group
+    const bool live = trel >= 0 && trel < (int)it.ngrp;
     uint32_t sp[4 * C::V];
 #pragma unroll
     for (int k = 0; k < 4 * C::V; ++k) {

@@ -34,6 +34,10 @@ QFS_HD constexpr int qrowbase(int deg, int a1, int a2)
 }
 QFS_HD constexpr int qround16(int n) { return (n + 15) & ~15; }
 
+#ifndef QFS_PITCH_ALIGN
+#define QFS_PITCH_ALIGN 128
+#endif
+
 template <int P>
 struct Shape {
     static constexpr int p = P;
@@ -46,7 +50,7 @@ struct Shape {
     static constexpr int Nh = qc3(dh + 3);
     static constexpr int NE = qc3(dE + 3);
     static constexpr int L = qc3(D + 3);
-    static constexpr int pitch = qround16(N);   // row pitch of M and stride of N-vectors
+    static constexpr int pitch = (N + QFS_PITCH_ALIGN - 1) / QFS_PITCH_ALIGN * QFS_PITCH_ALIGN;   // row pitch of M and stride of N-vectors
     static constexpr int Nh_pad = qround16(Nh);
     static constexpr int NE_pad = qround16(NE);
     static constexpr int L_pad = qround16(L);
