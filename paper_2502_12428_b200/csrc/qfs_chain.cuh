@@ -134,3 +134,129 @@ k_chain(const uint8_t* __restrict__ M_all, const uint8_t* __restrict__ v0_all, c
         }
     }
 }
+
+// ---- the same chain with the WHOLE GRID on one surface at a time ---------------------------------------------
+// k_chain gives a surface to one CTA; that is the right shape when thousands of surfaces are pending (p <= 7
+// batches), and the wrong one when a chunk holds a few dozen long surfaces (p >= 11: <= 460 matrices of 152 MB
+// per chunk, ~1/p of them undecided after the fused first step -- 40 busy CTAs of 148 streamed at 1.0-1.4 TB/s)
+// or when the caller asks for one surface (height_matrix of a single quartic).  Here every warp of a cooperative
+// grid owns the rows gw, gw + GW, ... of the current surface (GW = warps in the grid), streams each row with
+// KCH 16-byte loads in flight per lane, and the new vector goes through a 2 x pitch global scratch (L2) and a
+// grid barrier per step.  Same arithmetic, same results; the early exit is taken by all CTAs together.
+#include <cooperative_groups.h>
+
+template <int P>
+struct ChainGridCfg {
+    using S = Shape<P>;
+    static constexpr int NT = 1024;
+    static constexpr int KCH = 4;            // 16-byte loads in flight per lane
+    static constexpr int MAXCOUNT = 4096;    // surfaces per launch (one flag byte each in shared memory)
+    static constexpr int SMEM = S::pitch + MAXCOUNT;
+};
+
+template <int P>
+__global__ void __launch_bounds__(ChainGridCfg<P>::NT, 1)
+k_chain_grid(const uint8_t* __restrict__ M_all, const uint8_t* __restrict__ v0_all, const uint32_t* __restrict__ list,
+             int count, int start_it, int max_steps, uint8_t* __restrict__ trace, int8_t* __restrict__ heights,
+             int8_t* __restrict__ iters, uint8_t* __restrict__ scratch)
+{
+    namespace cg = cooperative_groups;
+    using S = Shape<P>;
+    using C = ChainGridCfg<P>;
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ __align__(16) uint8_t smem[];
+    uint8_t* sv = smem;                 // the current vector, pad bytes zero
+    uint8_t* sflag = smem + S::pitch;   // v0[slot][cap] of every slot of the launch
+    const int tid = threadIdx.x, lane = tid & 31;
+    // consecutive rows go to different CTAs: every SM streams the same number of rows (+-1)
+    const int gw = (tid >> 5) * gridDim.x + blockIdx.x, GW = gridDim.x * (C::NT / 32);
+    constexpr int NCH = S::pitch / 16;
+
+    for (int i = tid; i < count; i += C::NT) sflag[i] = start_it > 0 ? v0_all[(size_t)i * S::pitch + S::cap] : 0;
+    __syncthreads();
+    int par = 0;
+    for (int slot = 0; slot < count; ++slot) {
+        const uint32_t sid = list ? list[slot] : (uint32_t)slot;
+        if (start_it > 0 && (sflag[slot] != 0 || max_steps <= start_it)) {  // decided by the fused first step
+            if (blockIdx.x == 0 && tid == 0) {
+                heights[sid] = (int8_t)(sflag[slot] != 0 ? start_it + 1 : 0);
+                iters[sid] = (int8_t)start_it;
+            }
+            continue;
+        }
+        const uint8_t* M = M_all + (size_t)slot * ((size_t)S::N * S::pitch);
+        __syncthreads();  // everyone is done with the previous surface's vector
+        {
+            const uint4* src = reinterpret_cast<const uint4*>(v0_all + (size_t)slot * S::pitch);
+            for (int i = tid; i < NCH; i += C::NT) {
+                uint4 x = src[i];
+                if (16 * i + 16 > S::N) {  // pad bytes of a vector are never written by its producer: mask them
+                    uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                    for (int b = 0; b < 16; ++b)
+                        if (16 * i + b >= S::N) w[b >> 2] &= ~(0xFFu << (8 * (b & 3)));
+                    x = make_uint4(w[0], w[1], w[2], w[3]);
+                }
+                reinterpret_cast<uint4*>(sv)[i] = x;
+            }
+        }
+        __syncthreads();
+        int height = 0, it = start_it;
+        for (int step = start_it + 1; step <= max_steps; ++step) {
+            uint8_t* nxt = scratch + (size_t)par * S::pitch;
+            for (int row = gw; row < S::N; row += GW) {
+                const uint4* mrow = reinterpret_cast<const uint4*>(M + (size_t)row * S::pitch);
+                uint32_t acc = 0;
+                int ch0 = 0;
+                for (; ch0 + 32 * C::KCH <= NCH; ch0 += 32 * C::KCH) {
+                    uint4 m[C::KCH];
+#pragma unroll
+                    for (int k = 0; k < C::KCH; ++k) m[k] = ld_stream16(mrow + ch0 + 32 * k + lane);
+#pragma unroll
+                    for (int k = 0; k < C::KCH; ++k) {
+                        const uint4 v = reinterpret_cast<const uint4*>(sv)[ch0 + 32 * k + lane];
+                        acc = __dp4a(m[k].x, v.x, acc);
+                        acc = __dp4a(m[k].y, v.y, acc);
+                        acc = __dp4a(m[k].z, v.z, acc);
+                        acc = __dp4a(m[k].w, v.w, acc);
+                    }
+                }
+                for (int ch = ch0 + lane; ch < NCH; ch += 32) {
+                    const uint4 m = ld_stream16(mrow + ch);
+                    const uint4 v = reinterpret_cast<const uint4*>(sv)[ch];
+                    acc = __dp4a(m.x, v.x, acc);
+                    acc = __dp4a(m.y, v.y, acc);
+                    acc = __dp4a(m.z, v.z, acc);
+                    acc = __dp4a(m.w, v.w, acc);
+                }
+#pragma unroll
+                for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                if (lane == 0) nxt[row] = (uint8_t)(acc % (uint32_t)P);
+            }
+            grid.sync();  // the new vector is complete (and everyone has finished reading the old one)
+            for (int i = tid; i < NCH; i += C::NT) {
+                uint4 x = __ldcg(reinterpret_cast<const uint4*>(nxt) + i);
+                if (16 * i + 16 > S::N) {
+                    uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                    for (int b = 0; b < 16; ++b)
+                        if (16 * i + b >= S::N) w[b >> 2] &= ~(0xFFu << (8 * (b & 3)));
+                    x = make_uint4(w[0], w[1], w[2], w[3]);
+                }
+                reinterpret_cast<uint4*>(sv)[i] = x;
+            }
+            par ^= 1;  // the next step writes the other half: nobody can still be reading it (one barrier ago)
+            __syncthreads();
+            ++it;
+            if (trace && blockIdx.x == 0) {
+                uint8_t* tr = trace + ((size_t)slot * max_steps + (step - 1)) * S::N;
+                for (int i = tid; i < S::N; i += C::NT) tr[i] = sv[i];
+            }
+            if (sv[S::cap] != 0) { height = step + 1; break; }
+        }
+        if (blockIdx.x == 0 && tid == 0) {
+            heights[sid] = (int8_t)height;
+            iters[sid] = (int8_t)it;
+        }
+    }
+}

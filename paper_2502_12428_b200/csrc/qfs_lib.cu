@@ -62,6 +62,8 @@ struct qfs_ctx {
     size_t workspace_limit = 0;
     size_t auto_limit = 0;                          // default workspace budget, fixed at first use
     size_t chunk_override = 0;
+    int chain_grid_mode = -1;   // QFS_CHAIN_GRID: -1 automatic, 0 never, 1 always (k_chain_grid vs k_chain)
+    int chain_grid_ctas = 0;
     std::string error;
     qfs_stats stats = {};
     // device state
@@ -70,6 +72,7 @@ struct qfs_ctx {
     DevBuf unrank;                                  // per-p unrank tables for the power chain
     DevBuf coeffs, heights, iters, list;            // batch-sized
     DevBuf g, h, A, E, delta, M, v1;                // chunk-sized
+    DevBuf chain_scratch;                           // 2 x pitch: the vector exchange of k_chain_grid
     DevBuf tapA, tapB;                              // staging for the stage taps
     DevBuf items, vacc;                             // staged matrix builder: panel work list, 32-bit v1 accumulators
     int n_items = 0;
@@ -266,6 +269,7 @@ int build_tables(qfs_ctx* ctx)
     CU(cudaFuncSetAttribute(k_delta_direct<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, DeltaDirectCfg<P>::SMEM));
     CU(cudaFuncSetAttribute(k_free<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, FreeCfg<P>::SMEM));
     ctx->delta_direct = getenv("QFS_DELTA_DIRECT") ? 1 : 0;
+    if (const char* e = getenv("QFS_CHAIN_GRID")) ctx->chain_grid_mode = atoi(e);
     CU(cudaFuncSetAttribute(k_chain<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, ChainCfg<P>::SMEM));
     return QFS_OK;
 }
@@ -392,6 +396,29 @@ template <int P>
 int launch_chain(qfs_ctx* ctx, const uint8_t* v0, const uint32_t* d_list, int count, int start_it, int max_steps,
                  uint8_t* trace, int8_t* heights, int8_t* iters)
 {
+    // Few, long surfaces (p >= 11 chunks, single-surface calls): the whole grid on one surface at a time
+    // (k_chain_grid); otherwise one surface per persistent CTA (k_chain).  QFS_CHAIN_GRID=0/1 forces either.
+    using G = ChainGridCfg<P>;
+    const long expected = start_it > 0 ? count / P : count;  // surfaces the fused first step leaves undecided
+    bool use_grid = count <= G::MAXCOUNT && 2 * expected < (long)ctx->sm_count * ChainCfg<P>::CTAS_PER_SM;
+    if (ctx->chain_grid_mode >= 0) use_grid = ctx->chain_grid_mode > 0 && count <= G::MAXCOUNT;
+    if (use_grid) {
+        if (!ctx->chain_grid_ctas) {
+            int per_sm = 0;
+            CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_chain_grid<P>, G::NT, G::SMEM));
+            if (per_sm < 1) return fail(ctx, QFS_ECUDA, "k_chain_grid does not fit an SM");
+            ctx->chain_grid_ctas = ctx->sm_count;  // one 1024-thread CTA per SM
+        }
+        CU(ctx->chain_scratch.reserve(2 * (size_t)Shape<P>::pitch));
+        const uint8_t* M = ctx->M.as<uint8_t>();
+        uint8_t* scratch = ctx->chain_scratch.as<uint8_t>();
+        void* args[] = {(void*)&M, (void*)&v0, (void*)&d_list, (void*)&count, (void*)&start_it, (void*)&max_steps,
+                        (void*)&trace, (void*)&heights, (void*)&iters, (void*)&scratch};
+        CU(cudaLaunchCooperativeKernel((const void*)k_chain_grid<P>, dim3((unsigned)ctx->chain_grid_ctas), dim3(G::NT), args,
+                                       (size_t)G::SMEM, ctx->stream));
+        ctx->stats.kernel_launches++;
+        return QFS_OK;
+    }
     int* d_queue = ctx->flags.as<int>() + 1;
     CU(cudaMemsetAsync(d_queue, 0, sizeof(int), ctx->stream));
     const int grid = std::min(count, ctx->sm_count * ChainCfg<P>::CTAS_PER_SM);
@@ -762,7 +789,7 @@ void qfs_destroy(qfs_ctx* ctx)
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     DevBuf* bufs[] = {&ctx->flags, &ctx->colinfo, &ctx->groups, &ctx->runs, &ctx->unrank, &ctx->coeffs, &ctx->heights, &ctx->iters, &ctx->list,
-                      &ctx->g, &ctx->h, &ctx->A, &ctx->E, &ctx->delta, &ctx->M, &ctx->v1, &ctx->tapA, &ctx->tapB, &ctx->items, &ctx->vacc};
+                      &ctx->g, &ctx->h, &ctx->A, &ctx->E, &ctx->delta, &ctx->M, &ctx->v1, &ctx->tapA, &ctx->tapB, &ctx->items, &ctx->vacc, &ctx->chain_scratch};
     for (DevBuf* b : bufs) b->release();
     for (auto& e : ctx->ev) if (e) cudaEventDestroy(e);
     for (auto& e : ctx->ev_total) if (e) cudaEventDestroy(e);
@@ -935,7 +962,7 @@ int qfs_debug_fill_workspaces(qfs_ctx* ctx, int byte)
     if (!ctx) return QFS_EINVAL;
     CU(cudaSetDevice(ctx->device));
     DevBuf* bufs[] = {&ctx->g, &ctx->h, &ctx->A, &ctx->E, &ctx->delta, &ctx->M, &ctx->v1, &ctx->vacc, &ctx->tapA, &ctx->tapB,
-                      &ctx->coeffs, &ctx->heights, &ctx->iters, &ctx->list};
+                      &ctx->coeffs, &ctx->heights, &ctx->iters, &ctx->list, &ctx->chain_scratch};
     for (DevBuf* b : bufs)
         if (b->ptr) CU(cudaMemsetAsync(b->ptr, byte, b->cap, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));

@@ -81,6 +81,35 @@ def test_direct_witt_carry_kernel_equals_the_slab_kernel(p, monkeypatch):
         eng.close()
 
 
+@pytest.mark.parametrize("p", [3, 5, 7, 11])
+def test_both_chain_kernels_agree(p, monkeypatch):
+    """k_chain (a surface per persistent CTA) and k_chain_grid (the whole cooperative grid on one surface at a time,
+    chosen automatically for few long surfaces) against each other and the golden traces: heights, iteration counts
+    and every intermediate vector."""
+    import paper_2502_12428_b200 as q
+    from paper_2502_12428_b200.engine import Engine
+    big = q.sample_block(p, {3: 4000, 5: 3000, 7: 1500, 11: 700}[p], 31, 0)
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("QFS_CHAIN_GRID", mode)
+        eng = Engine(p, 0)
+        try:
+            out[mode] = eng.heights(big, 10)
+            if p <= 5:
+                z = np.load(os.path.join(GOLDEN, f"stages_p{p}.npz"))
+                idx = [i for i in range(int(z["count"])) if f"s{i}_M" in z.files]
+                M = np.stack([z[f"s{i}_M"] for i in idx])
+                g = np.stack([z[f"s{i}_g"] for i in idx])
+                hs, its, tr = eng.stage_matvec_chain(M, g, 9, trace=True)
+                for k, i in enumerate(idx):
+                    assert int(hs[k]) == int(z[f"s{i}_height"]) and int(its[k]) == int(z[f"s{i}_iters"])
+                    assert np.array_equal(tr[k][: its[k]], z[f"s{i}_trace"])
+        finally:
+            eng.close()
+    assert np.array_equal(out["0"][0], out["1"][0]) and np.array_equal(out["0"][1], out["1"][1])
+    assert (out["0"][0] > 2).sum() + (out["0"][0] == 0).sum() > 0  # the chain kernels did run
+
+
 def test_run_search_on_gpu_matches_reference():
     import paper_2502_12428_b200 as q
     z = np.load(os.path.join(GOLDEN, "heights_p5_seed0_w0_10000.npz"))
