@@ -54,7 +54,10 @@ __device__ __forceinline__ void st_shared_u8_le(uint32_t addr, uint32_t v, int a
 template <int P>
 struct DeltaCfg {
     using S = Shape<P>;
-    static constexpr int NT = (P >= 11) ? 512 : (P >= 7 ? 512 : (P >= 5 ? 256 : 64));
+#ifndef QFS_DELTA_NT11
+#define QFS_DELTA_NT11 512
+#endif
+    static constexpr int NT = (P >= 11) ? QFS_DELTA_NT11 : (P >= 7 ? 512 : (P >= 5 ? 256 : 64));
     static constexpr bool USE_BOX = (P < 7);   // p >= 7: no box (h is read with bounds checks): at p = 7 its 24 KB buy a fourth slab per phase instead
     static constexpr bool A_IN_SMEM = (P < 11);
     static constexpr int SB = S::dh + 9;       // box side: 4 zeros below, 4 above

@@ -399,8 +399,12 @@ int launch_chain(qfs_ctx* ctx, const uint8_t* v0, const uint32_t* d_list, int co
     // Few, long surfaces (p >= 11 chunks, single-surface calls): the whole grid on one surface at a time
     // (k_chain_grid); otherwise one surface per persistent CTA (k_chain).  QFS_CHAIN_GRID=0/1 forces either.
     using G = ChainGridCfg<P>;
-    const long expected = start_it > 0 ? count / P : count;  // surfaces the fused first step leaves undecided
-    bool use_grid = count <= G::MAXCOUNT && 2 * expected < (long)ctx->sm_count * ChainCfg<P>::CTAS_PER_SM;
+    // Cost model: the grid kernel pays a grid barrier (~3 us) plus N*pitch bytes at full bandwidth per step, a lone
+    // CTA of k_chain streams ~50 GB/s; above half the CTA slots k_chain reaches full bandwidth by itself.
+    const double expected = start_it > 0 ? (double)count / P : (double)count;  // surfaces the fused first step leaves undecided
+    const double mbytes = (double)Shape<P>::N * Shape<P>::pitch;
+    const double breakeven = (mbytes / 50e9) / (3e-6 + mbytes / 6e12);
+    bool use_grid = count <= G::MAXCOUNT && expected < std::min(breakeven, 0.5 * ctx->sm_count * ChainCfg<P>::CTAS_PER_SM);
     if (ctx->chain_grid_mode >= 0) use_grid = ctx->chain_grid_mode > 0 && count <= G::MAXCOUNT;
     if (use_grid) {
         if (!ctx->chain_grid_ctas) {

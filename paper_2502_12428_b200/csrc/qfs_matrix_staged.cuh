@@ -44,7 +44,22 @@ struct StagedCfg {
 #ifndef QFS_NT7
 #define QFS_NT7 192
 #endif
-    static constexpr int NT = (P >= 13) ? 384 : (P == 7 ? QFS_NT7 : (P >= 5 ? 256 : 64));  // consumer threads (p = 13: block c1 = 0 alone is 154 word groups; p = 7: 96-thread teams fit its ~91-group panels)
+#ifndef QFS_NT11
+#define QFS_NT11 256
+#endif
+#ifndef QFS_SLICE7
+#define QFS_SLICE7 8
+#endif
+#ifndef QFS_SLICE11
+#define QFS_SLICE11 8
+#endif
+#ifndef QFS_BUDGET7
+#define QFS_BUDGET7 12800
+#endif
+#ifndef QFS_BUDGET11
+#define QFS_BUDGET11 20480
+#endif
+    static constexpr int NT = (P >= 13) ? 384 : (P == 11 ? QFS_NT11 : (P == 7 ? QFS_NT7 : (P >= 5 ? 256 : 64)));  // consumer threads (p = 13: block c1 = 0 alone is 154 word groups; p = 7: 96-thread teams fit its ~91-group panels)
     static constexpr int TEAM = NT / TEAMS;                  // threads (= word groups) per team
     static constexpr int NTL = NT + 32;                      // launched: + the producer warp
     static constexpr int WORDS = S::pitch / 4;
@@ -56,10 +71,10 @@ struct StagedCfg {
     static constexpr int LINEG = (QFS_PITCH_ALIGN % 128 == 0) ? 128 / (4 * V) : 1;
     static constexpr int HEADRUNS = (V == 1) ? 2 : (V == 2 ? 4 : 5);  // runs covering the 4V-1 columns before a block
     static constexpr int MAXROWS = S::d + 1;
-    static constexpr int SLICE = (P >= 11) ? 8 : (P >= 7 ? 8 : 16);        // quads per CTA
+    static constexpr int SLICE = (P >= 11) ? QFS_SLICE11 : (P >= 7 ? QFS_SLICE7 : 16);        // quads per CTA
     static constexpr int ZW = (P * S::d + 4 + 3) & ~3;       // zero region (entries) read by columns that never match
     static constexpr int MAXC = S::d + 2;                    // pieces per panel
-    static constexpr int BUDGET = (P >= 13) ? 36864 : (P >= 11 ? 20480 : 12800);  // default staged entries (x4 bytes) per panel
+    static constexpr int BUDGET = (P >= 13) ? 36864 : (P >= 11 ? QFS_BUDGET11 : (P == 7 ? QFS_BUDGET7 : 12800));  // default staged entries (x4 bytes) per panel
     static constexpr size_t MSTRIDE = (size_t)S::N * S::pitch;
     static constexpr int VSEG = MAXG * 4 * V + 16;           // bytes of one surface's slice of v0 staged per buffer (16-byte aligned window)
     static constexpr int VWORDS = 4 * VSEG / 4;              // 32-bit words of the v0 area at the end of a buffer
