@@ -264,6 +264,32 @@ def measure_gpu(p, batch, steps, warmup, seed, rank, world, device, dist):
             "heights": heights, "iters": iters, "coeffs": host, "clocks": clocks}
 
 
+def measure_single_surface(device, results):
+    """BASELINE.json configs[0]: ONE quartic through the public call with host buffers (wall clock, median of 20), for the
+    surface of the seeded batch with the most operator applications, next to the CPU oracle on one thread."""
+    import oracle
+    from paper_2502_12428_b200.engine import get_engine
+    out = {}
+    for p, res in results.items():
+        i = int(np.argmax(res["iters"]))
+        one = np.ascontiguousarray(res["coeffs"][i:i + 1])
+        eng = get_engine(p, device)
+        ts = []
+        for k in range(23):
+            t0 = time.perf_counter()
+            h, it = eng.heights(one, 10)
+            if k >= 3:
+                ts.append(time.perf_counter() - t0)
+        t0 = time.perf_counter()
+        oh, oit = oracle.heights_batch(one, p, 10, 1)
+        cpu_s = time.perf_counter() - t0
+        out[f"F_{p}"] = {"ms_per_call": 1e3 * float(np.median(ts)), "height": int(h[0]), "iterations": int(it[0]),
+                         "cpu_oracle_ms": 1e3 * cpu_s, "cpu_cores": 1,
+                         "equals_oracle": bool(int(oh[0]) == int(h[0]) and int(oit[0]) == int(it[0])),
+                         "surface": f"index {i} of the seeded batch", "stage_ms": {k: v for k, v in eng.stats().items() if k.startswith("ms_")}}
+    return out
+
+
 def measure_matrix_free(device, seed, checked):
     """surfaces/s of qfs_heights_free on resident inputs (CUDA events), F_5 ... F_13, 100000 seeded quartics each;
     for the primes in `checked` the heights and iteration counts are compared with the matrix path's."""
@@ -311,7 +337,7 @@ def gpu_line(args, p, res, world, with_cpu):
     stage = {k: v / steps for k, v in res["stage"].items()}
     kernels = {"delta": ("k_delta", stage["ms_delta"], ab["delta"]),
                "matrix": ("k_matrix_staged", stage["ms_matrix"], ab["matrix"]),
-               "matvec": ("k_chain", stage["ms_matvec"], ab["matvec"])}
+               "matvec": ("k_chain" if p <= 7 else "k_chain_grid", stage["ms_matvec"], ab["matvec"])}
     top = max(kernels, key=lambda k: kernels[k][1])
     name, kms, kbytes = kernels[top]
     ach = kbytes / (kms * 1e-3) / 1e9 if kms > 0 else 0.0
@@ -419,6 +445,7 @@ def main():
         # path (the north star requires the operator matrix in HBM and the streamed matvec chain): reported beside it.
         if rank == 0 and world == 1:
             line["also"]["matrix_free"] = measure_matrix_free(local, args.seed, {5: res, 7: res7})
+            line["also"]["single_surface"] = measure_single_surface(local, {5: res, 7: res7})
     if rank == 0:
         print(json.dumps(line))
     if dist is not None:

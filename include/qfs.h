@@ -53,7 +53,7 @@ typedef struct qfs_shape {
     int32_t d;       /* deg f^(p-1) = 4(p-1)                       */
     int32_t D;       /* deg Delta_1(f^(p-1)) = 4p(p-1)             */
     int32_t N;       /* C(4p-1,3): operator dimension              */
-    int32_t pitch;   /* internal row pitch of M in bytes (N rounded up to 16) */
+    int32_t pitch;   /* internal row pitch of M in bytes (N rounded up to 128: rows start on 128-byte lines) */
     int32_t cap;     /* index of (x1x2x3x4)^(p-1) in basis(d,4)    */
     int64_t L;       /* C(D+3,3): dense length of Delta            */
 } qfs_shape;

@@ -9,7 +9,7 @@
 //     M[r, c] = Delta[p*r + (p-1) - c]      if every component is >= 0, else 0,
 // for r, c in basis(d,4), d = 4(p-1).  No atomics, no hash table, no index search.
 //
-// Layout.  M is row-major with pitch = N rounded up to 16 bytes (pad columns are zero), one byte
+// Layout.  M is row-major with pitch = N rounded up to 128 bytes (pad columns are zero), one byte
 // per entry (residues < p).  With Delta in "lex43g" order (qfs_shape.cuh) a column run (c1,c2,*)
 // of row r = (r1,r2,r3,r4) is a forward copy:
 //     M[r, (c1,c2,c3)] = Delta43g[ gbase(I1,I2) + I4 ],  I1 = p r1+p-1-c1, I2 = p r2+p-1-c2,

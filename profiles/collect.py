@@ -88,7 +88,9 @@ json.dump(traffic, open(os.path.join(HERE, "traffic.json"), "w"), indent=1)
 d = json.loads(open(os.path.join(HERE, f"{tag}_bench_line.json")).read().strip().splitlines()[-1])
 print("F_5", round(d["value"]), {k: round(v, 3) for k, v in d["stage_ms_per_step"].items()}, "frac", round(d["roofline"]["frac"], 3), "e2e", round(d["e2e"]["value"]))
 for k, a in d["also"].items():
-    if k != "matrix_free":
+    if k == "single_surface":
+        print(k, {kk: (round(v["ms_per_call"], 3), round(v["cpu_oracle_ms"], 1)) for kk, v in a.items()})
+    elif k != "matrix_free":
         print(k, round(a["value"]), {kk: round(v, 3) for kk, v in a["stage_ms_per_step"].items()}, "frac", round(a["roofline"]["frac"], 3), "e2e", round(a["e2e"]["value"]))
     else:
         print(k, {kk: round(v["value"]) for kk, v in a.items() if kk != "note"})
