@@ -203,46 +203,48 @@ int build_tables(qfs_ctx* ctx)
     }
     {   // panels of the staged matrix builder (qfs_matrix_staged.cuh)
         using SC = StagedCfg<P>;
-        std::vector<int> c1g(SC::NGRP);  // block c1 of the last valid column of each word group of a row
-        for (int g = 0; g < SC::NGRP; ++g) c1g[g] = (int)(col[std::min(4 * SC::V * (g + 1) - 1, S::N - 1)] & 255);
         int budget = SC::BUDGET;
         if (const char* e = getenv("QFS_STAGED_BUDGET")) budget = std::max(SC::BUDGET / 8, atoi(e));
         struct Tmp { PanelItem it; long work; int staged; };
         std::vector<Tmp> tmp;
         int max_staged = 0;
-        const int last_start = std::max(0, S::d + 2 - SC::HEADRUNS);  // a panel may start at block lo only if block lo-1 holds the head runs
+        // A panel = word groups [ga, gb) of the rows of one row group; ga and gb are multiples of LINEG (whole
+        // 128-byte lines) except at the row end.  Its columns [first, last] run from (c1lo, c2lo, .) to (c1hi, c2hi, .).
+        constexpr int CPG = 4 * SC::V;  // columns per word group
         for (int r1 = 0; r1 <= S::d; ++r1)
             for (int r2 = 0; r1 + r2 <= S::d; ++r2) {
-                auto piece = [&](int c1, int c2min) { int a4, b4; return staged_piece<P>(r1, r2, c1, c2min, a4, b4) ? b4 - a4 : 0; };
-                auto groups_of = [&](int lo, int hi, int& glo) {
-                    int n = 0; glo = -1;
-                    for (int g = 0; g < SC::NGRP; ++g) if (c1g[g] >= lo && c1g[g] <= hi) { if (glo < 0) glo = g; ++n; }
-                    return n;
-                };
-                auto staged_of = [&](int lo, int hi) {
-                    int st = (lo > 0) ? piece(lo - 1, staged_head_c2min<P>(lo - 1)) : 0;
-                    for (int c1 = lo; c1 <= hi; ++c1) st += piece(c1, 0);
+                auto make = [&](int ga, int gb, PanelItem& it) {  // returns the staged entries of the panel, -1 if it has no column
+                    const int first = CPG * ga, last = std::min(CPG * gb, S::N) - 1;
+                    if (first > last) return -1;
+                    const int c1lo = (int)(col[first] & 255), c2lo = (int)((col[first] >> 8) & 255);
+                    const int c1hi = (int)(col[last] & 255), c2hi = (int)((col[last] >> 8) & 255);
+                    int st = 0;
+                    for (int c1 = c1lo; c1 <= c1hi; ++c1) {
+                        int a4, b4;
+                        if (staged_piece<P>(r1, r2, c1, c1 == c1lo ? c2lo : 0, c1 == c1hi ? c2hi : S::d - c1, a4, b4)) st += b4 - a4;
+                    }
+                    it = PanelItem{(uint8_t)r1, (uint8_t)r2, (uint8_t)c1lo, (uint8_t)c1hi, (uint16_t)ga, (uint16_t)(gb - ga),
+                                   (uint8_t)c2lo, (uint8_t)c2hi, 0};
                     return st;
                 };
-                int lo = 0;
-                while (lo <= S::d) {
-                    int dummy;
-                    auto fits = [&](int h) {
-                        const int n = groups_of(lo, h, dummy);
-                        return staged_of(lo, h) <= budget && (n == 0 || dummy % SC::LINEG + n <= SC::MAXG);
-                    };
-                    int hi = lo;
-                    while (hi < S::d && fits(hi + 1)) ++hi;
-                    if (hi >= last_start && hi < S::d) hi = last_start - 1;  // the tail blocks stay together
-                    if (hi < lo || !fits(hi)) return fail(ctx, QFS_EINVAL, "internal: panel does not fit the shared-memory budget");
-                    int glo, n = groups_of(lo, hi, glo);
-                    if (n > 0) {
-                        const int st = staged_of(lo, hi);
-                        PanelItem it{(uint8_t)r1, (uint8_t)r2, (uint8_t)lo, (uint8_t)hi, (uint16_t)glo, (uint16_t)n};
-                        tmp.push_back({it, (long)n * (S::d - r1 - r2 + 1), st});
-                        max_staged = std::max(max_staged, st);
+                const int gend = (S::N + CPG - 1) / CPG;  // word groups that hold a column; the pad groups go with the last panel
+                int ga = 0;
+                while (ga < gend) {
+                    PanelItem it{}, best{};
+                    int best_st = -1, gb = ga;
+                    while (gb < SC::NGRP) {
+                        int nb = std::min(SC::NGRP, gb + SC::LINEG);
+                        if (nb >= gend) nb = SC::NGRP;
+                        if (nb - ga > SC::MAXG) break;
+                        const int st = make(ga, nb, it);
+                        if (st > budget && best_st >= 0) break;
+                        if (st > budget) return fail(ctx, QFS_EINVAL, "internal: panel does not fit the shared-memory budget");
+                        best = it; best_st = st; gb = nb;
                     }
-                    lo = hi + 1;
+                    if (best_st < 0) return fail(ctx, QFS_EINVAL, "internal: panel does not fit the shared-memory budget");
+                    tmp.push_back({best, (long)best.ngrp * (S::d - r1 - r2 + 1), best_st});
+                    max_staged = std::max(max_staged, best_st);
+                    ga = gb;
                 }
             }
         // Launch order = memory order of the rows (r1, r2 lexicographic, panels of a group adjacent): CTAs that

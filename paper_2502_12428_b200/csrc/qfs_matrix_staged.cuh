@@ -13,10 +13,12 @@
 // What is staged.  For a row group (r1,r2) the sources of the column block c1 (all c2, c3) are the
 // Delta runs (I1, I2lo..I2hi), I1 = p r1+p-1-c1, I2 = p r2+p-1-c2: ONE contiguous piece of the
 // guard-banded lex43g array (qfs_shape.cuh), because runs are ordered by (I1, I2).  A work item
-// ("panel") = (r1, r2, c1lo..c1hi): it stages the pieces of its column blocks (plus the last
-// HEADRUNS runs of block c1lo-1, which its first word group may straddle) and writes, for every
-// row of the group, the word groups (V x 32 bits) whose LAST column lies in its blocks.  The host
-// cuts every row group into panels that fit the shared-memory budget (p = 3, 5: one per group).
+// ("panel") = (r1, r2, word groups [glo, glo+ngrp) of the rows): a column range whose ends sit on
+// 128-byte lines of the row (tools/micro/write_bw4.cu: segments that share no line with a neighbour
+// panel write 1.2-1.8x faster).  It stages, for every column block c1 its columns touch, the piece
+// restricted to the c2 it needs (first block: c2 >= c2lo, last block: c2 <= c2hi) and writes its word
+// groups (V x 32 bits) of every row of the group.  The host cuts every row into panels that fit the
+// shared-memory budget (p = 3, 5: one per row group).
 //
 // CTA = NT consumer threads + one producer warp.  Consumers: thread = (row team, word group); the
 // V teams take the rows t = team, team+V, ...  Producer warp: issues the bulk copies of the next
@@ -29,8 +31,10 @@
 #include "qfs_shape.cuh"
 
 struct PanelItem {
-    uint8_t r1, r2, c1lo, c1hi;
-    uint16_t glo, ngrp;   // owned word groups of a row: [glo, glo + ngrp), in units of V 32-bit words
+    uint8_t r1, r2, c1lo, c1hi;   // row group; first and last column block the panel's columns touch
+    uint16_t glo, ngrp;           // owned word groups of a row: [glo, glo + ngrp), in units of V 32-bit words
+    uint8_t c2lo, c2hi;           // c2 of the panel's first column (in block c1lo) and of its last column (in block c1hi)
+    uint16_t pad;
 };
 
 template <int P>
@@ -69,7 +73,6 @@ struct StagedCfg {
     // panel's first word group, so that every warp store covers whole lines (tools/micro/write_bw4.cu); the
     // glo % LINEG threads in front of the panel repeat its first word group.
     static constexpr int LINEG = (QFS_PITCH_ALIGN % 128 == 0) ? 128 / (4 * V) : 1;
-    static constexpr int HEADRUNS = (V == 1) ? 2 : (V == 2 ? 4 : 5);  // runs covering the 4V-1 columns before a block
     static constexpr int MAXROWS = S::d + 1;
     static constexpr int SLICE = (P >= 11) ? QFS_SLICE11 : (P >= 7 ? QFS_SLICE7 : 16);        // quads per CTA
     static constexpr int ZW = (P * S::d + 4 + 3) & ~3;       // zero region (entries) read by columns that never match
@@ -122,29 +125,22 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity)
         : "memory");
 }
 
-// The piece of Delta that column block c1 of row group (r1,r2) reads, restricted to c2 >= c2min:
+// The piece of Delta that column block c1 of row group (r1,r2) reads, restricted to c2min <= c2 <= c2max:
 // entries [a, b) of the lex43g array (a rounded down, b rounded up to a multiple of 32 entries = 128 bytes
 // of the quad-interleaved array).  Returns false when no column of the block can match.
 template <int P>
-QFS_HD bool staged_piece(int r1, int r2, int c1, int c2min, int& a4, int& b4)
+QFS_HD bool staged_piece(int r1, int r2, int c1, int c2min, int c2max, int& a4, int& b4)
 {
     using S = Shape<P>;
     const int I1 = P * r1 + P - 1 - c1;
     if (I1 < 0 || I1 > S::D) return false;
-    int I2lo = P * r2 + P - 1 - (S::d - c1), I2hi = P * r2 + P - 1 - c2min;
+    int I2lo = P * r2 + P - 1 - c2max, I2hi = P * r2 + P - 1 - c2min;
     if (I2lo < 0) I2lo = 0;
     if (I2hi > S::D - I1) I2hi = S::D - I1;
     if (I2lo > I2hi) return false;
     a4 = (S::gbase(I1, I2lo) - S::G) & ~31;
     b4 = (S::gbase(I1, I2hi + 1) + 31) & ~31;
     return true;
-}
-// c2min of the head piece taken from block c1 = c1lo - 1
-template <int P>
-QFS_HD int staged_head_c2min(int c1)
-{
-    const int v = Shape<P>::d - c1 - (StagedCfg<P>::HEADRUNS - 1);
-    return v > 0 ? v : 0;
 }
 
 template <int V> struct StoreVec;
@@ -221,7 +217,7 @@ k_matrix_staged(const uint8_t* __restrict__ delta_all, const uint32_t* __restric
     const int nquads = (count + 3) >> 2;
     const int q_begin = blockIdx.y * C::SLICE;
     const int q_end = min(nquads, q_begin + C::SLICE);
-    const int cfirst = c1lo > 0 ? c1lo - 1 : 0;
+    const int cfirst = c1lo;
     const uint32_t sm_base = (uint32_t)__cvta_generic_to_shared(sm);
     const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(s_bar);
     const uint32_t bufbytes = 4u * (uint32_t)bufwords;
@@ -230,8 +226,8 @@ k_matrix_staged(const uint8_t* __restrict__ delta_all, const uint32_t* __restric
         int so = C::ZW, n = 0;
         for (int c1 = cfirst; c1 <= c1hi; ++c1) {
             int a4, b4, rel = INT_MIN;
-            const int c2min = (c1 < c1lo) ? staged_head_c2min<P>(c1) : 0;
-            if (staged_piece<P>(r1, r2, c1, c2min, a4, b4)) {
+            const int c2min = (c1 == c1lo) ? it.c2lo : 0, c2max = (c1 == c1hi) ? it.c2hi : S::d - c1;
+            if (staged_piece<P>(r1, r2, c1, c2min, c2max, a4, b4)) {
                 rel = so - a4;
                 s_cpa[n] = a4;
                 s_cpn[n] = 4 * (b4 - a4);  // bytes
