@@ -46,7 +46,16 @@ struct StagedCfg {
     static constexpr int V = (P >= 7) ? 2 : (P == 5 ? QFS_V5 : 1);                              // consecutive 32-bit words per thread (store width 4V bytes)
     static constexpr int TEAMS = V;                          // row teams
 #ifndef QFS_NT7
-#define QFS_NT7 192
+#define QFS_NT7 128
+#endif
+#ifndef QFS_NT5
+#define QFS_NT5 128
+#endif
+#ifndef QFS_BUDGET5
+#define QFS_BUDGET5 6400
+#endif
+#ifndef QFS_SLICE5
+#define QFS_SLICE5 16
 #endif
 #ifndef QFS_NT11
 #define QFS_NT11 256
@@ -58,12 +67,12 @@ struct StagedCfg {
 #define QFS_SLICE11 8
 #endif
 #ifndef QFS_BUDGET7
-#define QFS_BUDGET7 12800
+#define QFS_BUDGET7 8000
 #endif
 #ifndef QFS_BUDGET11
-#define QFS_BUDGET11 20480
+#define QFS_BUDGET11 16384
 #endif
-    static constexpr int NT = (P >= 13) ? 384 : (P == 11 ? QFS_NT11 : (P == 7 ? QFS_NT7 : (P >= 5 ? 256 : 64)));  // consumer threads (p = 13: block c1 = 0 alone is 154 word groups; p = 7: 96-thread teams fit its ~91-group panels)
+    static constexpr int NT = (P >= 13) ? 384 : (P == 11 ? QFS_NT11 : (P == 7 ? QFS_NT7 : (P >= 5 ? QFS_NT5 : 64)));  // consumer threads (p = 13: block c1 = 0 alone is 154 word groups; p = 7: 96-thread teams fit its ~91-group panels)
     static constexpr int TEAM = NT / TEAMS;                  // threads (= word groups) per team
     static constexpr int NTL = NT + 32;                      // launched: + the producer warp
     static constexpr int WORDS = S::pitch / 4;
@@ -74,10 +83,10 @@ struct StagedCfg {
     // glo % LINEG threads in front of the panel repeat its first word group.
     static constexpr int LINEG = (QFS_PITCH_ALIGN % 128 == 0) ? 128 / (4 * V) : 1;
     static constexpr int MAXROWS = S::d + 1;
-    static constexpr int SLICE = (P >= 11) ? QFS_SLICE11 : (P >= 7 ? QFS_SLICE7 : 16);        // quads per CTA
+    static constexpr int SLICE = (P >= 11) ? QFS_SLICE11 : (P >= 7 ? QFS_SLICE7 : QFS_SLICE5);        // quads per CTA
     static constexpr int ZW = (P * S::d + 4 + 3) & ~3;       // zero region (entries) read by columns that never match
     static constexpr int MAXC = S::d + 2;                    // pieces per panel
-    static constexpr int BUDGET = (P >= 13) ? 36864 : (P >= 11 ? QFS_BUDGET11 : (P == 7 ? QFS_BUDGET7 : 12800));  // default staged entries (x4 bytes) per panel
+    static constexpr int BUDGET = (P >= 13) ? 36864 : (P >= 11 ? QFS_BUDGET11 : (P == 7 ? QFS_BUDGET7 : (P == 5 ? QFS_BUDGET5 : 12800)));  // default staged entries (x4 bytes) per panel
     static constexpr size_t MSTRIDE = (size_t)S::N * S::pitch;
     static constexpr int VSEG = MAXG * 4 * V + 16;           // bytes of one surface's slice of v0 staged per buffer (16-byte aligned window)
     static constexpr int VWORDS = 4 * VSEG / 4;              // 32-bit words of the v0 area at the end of a buffer
