@@ -57,6 +57,12 @@ struct StagedCfg {
 #ifndef QFS_SLICE5
 #define QFS_SLICE5 16
 #endif
+#ifndef QFS_NT13
+#define QFS_NT13 256
+#endif
+#ifndef QFS_BUDGET13
+#define QFS_BUDGET13 24576
+#endif
 #ifndef QFS_NT11
 #define QFS_NT11 256
 #endif
@@ -72,7 +78,7 @@ struct StagedCfg {
 #ifndef QFS_BUDGET11
 #define QFS_BUDGET11 16384
 #endif
-    static constexpr int NT = (P >= 13) ? 384 : (P == 11 ? QFS_NT11 : (P == 7 ? QFS_NT7 : (P >= 5 ? QFS_NT5 : 64)));  // consumer threads (p = 13: block c1 = 0 alone is 154 word groups; p = 7: 96-thread teams fit its ~91-group panels)
+    static constexpr int NT = (P >= 13) ? QFS_NT13 : (P == 11 ? QFS_NT11 : (P == 7 ? QFS_NT7 : (P >= 5 ? QFS_NT5 : 64)));  // consumer threads (p = 13: block c1 = 0 alone is 154 word groups; p = 7: 96-thread teams fit its ~91-group panels)
     static constexpr int TEAM = NT / TEAMS;                  // threads (= word groups) per team
     static constexpr int NTL = NT + 32;                      // launched: + the producer warp
     static constexpr int WORDS = S::pitch / 4;
@@ -86,7 +92,7 @@ struct StagedCfg {
     static constexpr int SLICE = (P >= 11) ? QFS_SLICE11 : (P >= 7 ? QFS_SLICE7 : QFS_SLICE5);        // quads per CTA
     static constexpr int ZW = (P * S::d + 4 + 3) & ~3;       // zero region (entries) read by columns that never match
     static constexpr int MAXC = S::d + 2;                    // pieces per panel
-    static constexpr int BUDGET = (P >= 13) ? 36864 : (P >= 11 ? QFS_BUDGET11 : (P == 7 ? QFS_BUDGET7 : (P == 5 ? QFS_BUDGET5 : 12800)));  // default staged entries (x4 bytes) per panel
+    static constexpr int BUDGET = (P >= 13) ? QFS_BUDGET13 : (P >= 11 ? QFS_BUDGET11 : (P == 7 ? QFS_BUDGET7 : (P == 5 ? QFS_BUDGET5 : 12800)));  // default staged entries (x4 bytes) per panel
     static constexpr size_t MSTRIDE = (size_t)S::N * S::pitch;
     static constexpr int VSEG = MAXG * 4 * V + 16;           // bytes of one surface's slice of v0 staged per buffer (16-byte aligned window)
     static constexpr int VWORDS = 4 * VSEG / 4;              // 32-bit words of the v0 area at the end of a buffer
