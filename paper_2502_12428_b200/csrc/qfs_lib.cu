@@ -64,6 +64,7 @@ struct qfs_ctx {
     size_t chunk_override = 0;
     int chain_grid_mode = -1;   // QFS_CHAIN_GRID: -1 automatic, 0 never, 1 always (k_chain_grid vs k_chain)
     int chain_grid_ctas = 0;
+    int delta_wave = 0;         // CTAs of k_delta resident at a time (0: the direct kernel is used)
     std::string error;
     qfs_stats stats = {};
     // device state
@@ -271,6 +272,24 @@ int build_tables(qfs_ctx* ctx)
     CU(cudaFuncSetAttribute(k_delta_direct<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, DeltaDirectCfg<P>::SMEM));
     CU(cudaFuncSetAttribute(k_free<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, FreeCfg<P>::SMEM));
     ctx->delta_direct = getenv("QFS_DELTA_DIRECT") ? 1 : 0;
+    if constexpr (DeltaCfg<P>::SMEM <= 227 * 1024) {
+        // resident 4-CTA clusters (a GPC whose SM count is not a multiple of what a cluster needs leaves SMs idle)
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(4 * 1024);
+        cfg.blockDim = dim3(DeltaCfg<P>::NT);
+        cfg.dynamicSmemBytes = DeltaCfg<P>::SMEM;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 4;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int clusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&clusters, k_delta<P>, &cfg) != cudaSuccess) { cudaGetLastError(); clusters = 0; }
+        ctx->delta_wave = 4 * clusters;
+        if (getenv("QFS_VERBOSE")) fprintf(stderr, "qfs: p=%d resident k_delta clusters %d (%d SMs)\n", P, clusters, ctx->sm_count);
+    }
     if (const char* e = getenv("QFS_CHAIN_GRID")) ctx->chain_grid_mode = atoi(e);
     CU(cudaFuncSetAttribute(k_chain<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, ChainCfg<P>::SMEM));
     return QFS_OK;
@@ -523,6 +542,12 @@ int run_heights(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, int bound, int8_t
         const size_t per = matrix_free ? (size_t)(3 * S::pitch + S::Nh_pad + S::NE_pad) : per_surface_bytes<P>();
         size_t cap = ctx->chunk_override ? ctx->chunk_override : std::max<size_t>(1, limit / per);
         cap = std::min<size_t>(cap, (size_t)hard);
+        if (!matrix_free && !ctx->chunk_override && cap < (size_t)hard) {
+            // Few, large surfaces per chunk (p >= 11): a chunk of whole Witt-carry waves (one CTA per surface, delta_wave
+            // CTAs resident) avoids a partial last wave in every chunk (F_11: 460 -> 444 = 3 x 148; 80 -> 61 waves per 9016 surfaces)
+            const size_t wave = (size_t)ctx->delta_wave;
+            if (wave && cap >= wave && cap < 16 * wave) cap = cap / wave * wave;
+        }
         while (true) {
             int rc = matrix_free ? reserve_chunk_free<P>(ctx, cap) : reserve_chunk<P>(ctx, cap);
             if (rc == QFS_OK) break;
