@@ -425,6 +425,10 @@ def main():
         keep = ("value", "unit", "ms_per_step", "steps", "hard_per_s", "vs_baseline", "stage_ms_per_step", "roofline",
                 "roofline_pipeline", "e2e", "cpu_baseline", "height_histogram", "config")
         k7 = max(2, args.steps // 3)
+        # every configuration gets the device's memory to itself, as a user running it alone would: the engines of the
+        # previous configuration (and their HBM workspaces, which size the next engine's chunks) are closed first
+        from paper_2502_12428_b200.engine import close_all
+        close_all()
         res7 = measure_gpu(7, args.batch, k7, 3, args.seed, rank, world, local, dist)
         res7["steps"] = k7
         if rank == 0:
@@ -435,6 +439,7 @@ def main():
         b11 = min(args.batch, 4000)
         saved = args.batch
         args.batch = b11
+        close_all()
         res11 = measure_gpu(11, b11, 2, 3, args.seed, rank, world, local, dist)
         res11["steps"] = 2
         if rank == 0:

@@ -192,11 +192,15 @@ k_delta(const uint8_t* __restrict__ h_all, const uint8_t* __restrict__ A_all, co
     }
     __syncthreads();
 
-    // packed h neighbourhoods of the points of layer s1: sHp[w][q] byte b = h[s - t_j], j = 4w+b
-    auto build_hp = [&](int s1) {
+    // ---- slabs ---------------------------------------------------------------------------------
+#pragma unroll 1
+    for (int s1 = 0; s1 <= S::d; ++s1) {
+        const int I1 = P * s1;  // first slab of the layer
         const int ns = S::d - s1;
         const int T = (ns + 1) * (ns + 2) / 2;
-        for (int q = tid; q < (live ? T : 0); q += C::NT) {
+        {
+            // packed h neighbourhoods of the layer's points: sHp[w][q] byte b = h[s - t_j], j = 4w+b
+            for (int q = tid; q < (live ? T : 0); q += C::NT) {
                 const uint32_t e = sTri[q];
                 const int kk = e & 255, s2 = e >> 8, s3 = kk - s2;
                 uint32_t word = 0;
@@ -223,16 +227,8 @@ k_delta(const uint8_t* __restrict__ h_all, const uint8_t* __restrict__ A_all, co
                         }
                 sHp[8 * C::TPAD + q] = word;  // taps 32..34
             }
-    };
-    build_hp(0);
-    __syncthreads();
-
-    // ---- slabs ---------------------------------------------------------------------------------
-#pragma unroll 1
-    for (int s1 = 0; s1 <= S::d; ++s1) {
-        const int I1 = P * s1;  // first slab of the layer
-        const int ns = S::d - s1;
-        const int T = (ns + 1) * (ns + 2) / 2;
+            __syncthreads();
+        }
         for (int rho1_0 = 0; rho1_0 < P; rho1_0 += C::KS) {
         const int ks = min(C::KS, P - rho1_0);
         const int I1_0 = I1 + rho1_0;
@@ -306,11 +302,7 @@ k_delta(const uint8_t* __restrict__ h_all, const uint8_t* __restrict__ A_all, co
                 *reinterpret_cast<uint4*>(gq + 4 * (size_t)(x_lo + 4 * gi)) = make_uint4(out[0], out[1], out[2], out[3]);
             }
         }
-        // everyone must have read this CTA's slab before it is cleared: arrive now, wait after the next layer's sHp is built
-        // (sHp is read by this CTA's compute loop only, and all its threads are past the first cluster barrier)
-        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-        if (rho1_0 + C::KS >= P && s1 < S::d) build_hp(s1 + 1);
-        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+        cluster.sync();  // everyone has read this CTA's slab: clear it for the next phase
         for (int i = tid; i < (bytes + 15 + 15) >> 4; i += C::NT) reinterpret_cast<uint4*>(sSlab)[i] = make_uint4(0, 0, 0, 0);
         __syncthreads();
         }  // phases of the layer
