@@ -186,6 +186,21 @@ def test_large_batch_properties():
     assert np.array_equal(hs, hs3)
 
 
+def test_full_size_f7_batch_matrix_path_equals_matrix_free_iteration():
+    """BASELINE.json configs[2] at full size (100 000 seeded quartics over F_7, ~14 000 operator matrices of 8.6 MB, several
+    HBM chunks): the matrix path (Delta, M in HBM, streamed chain) and the matrix-free polynomial iteration are independent
+    routes to the same heights and iteration counts; the first 10 000 are the reference's own seeded golden set."""
+    import paper_2502_12428_b200 as q
+    c = q.sample_block(7, 100000, 0, 0)
+    hs, its = q.height_batch(7, c)
+    hf, itf = q.height_batch(7, c, method="naive")
+    assert np.array_equal(hs, hf) and np.array_equal(its, itf)
+    z = np.load(os.path.join(GOLDEN, "heights_p7_seed0_w0_10000.npz"))
+    assert np.array_equal(c[:10000], z["coeffs"])
+    assert np.array_equal(hs[:10000].astype(np.int64), z["heights"].astype(np.int64))
+    assert np.array_equal(its[:10000].astype(np.int64), z["iters"].astype(np.int64))
+
+
 @pytest.mark.parametrize("p", [3, 5, 7])
 def test_results_do_not_depend_on_what_the_workspaces_held(p):
     """Recycled device memory is not zero: poison every workspace between calls (qfs_debug_fill_workspaces)
