@@ -439,10 +439,16 @@ int launch_chain(qfs_ctx* ctx, const uint8_t* v0, const uint32_t* d_list, int co
         uint8_t* scratch = ctx->chain_scratch.as<uint8_t>();
         void* args[] = {(void*)&M, (void*)&v0, (void*)&d_list, (void*)&count, (void*)&start_it, (void*)&max_steps,
                         (void*)&trace, (void*)&heights, (void*)&iters, (void*)&scratch};
-        CU(cudaLaunchCooperativeKernel((const void*)k_chain_grid<P>, dim3((unsigned)ctx->chain_grid_ctas), dim3(G::NT), args,
-                                       (size_t)G::SMEM, ctx->stream));
-        ctx->stats.kernel_launches++;
-        return QFS_OK;
+        const cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_chain_grid<P>, dim3((unsigned)ctx->chain_grid_ctas),
+                                                          dim3(G::NT), args, (size_t)G::SMEM, ctx->stream);
+        if (e == cudaSuccess) {
+            ctx->stats.kernel_launches++;
+            return QFS_OK;
+        }
+        // a device partition that cannot hold one CTA per SM at once (MPS / green contexts): use the per-CTA kernel
+        if (e != cudaErrorCooperativeLaunchTooLarge && e != cudaErrorNotSupported) CU(e);
+        cudaGetLastError();
+        ctx->chain_grid_mode = 0;
     }
     int* d_queue = ctx->flags.as<int>() + 1;
     CU(cudaMemsetAsync(d_queue, 0, sizeof(int), ctx->stream));
