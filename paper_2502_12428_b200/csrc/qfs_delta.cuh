@@ -57,7 +57,13 @@ struct DeltaCfg {
 #ifndef QFS_DELTA_NT11
 #define QFS_DELTA_NT11 512
 #endif
-    static constexpr int NT = (P >= 11) ? QFS_DELTA_NT11 : (P >= 7 ? 512 : (P >= 5 ? 256 : 64));
+#ifndef QFS_DELTA_NT7
+#define QFS_DELTA_NT7 512
+#endif
+#ifndef QFS_DELTA_NT5
+#define QFS_DELTA_NT5 256
+#endif
+    static constexpr int NT = (P >= 11) ? QFS_DELTA_NT11 : (P >= 7 ? QFS_DELTA_NT7 : (P >= 5 ? QFS_DELTA_NT5 : 64));
     static constexpr bool USE_BOX = (P < 7);   // p >= 7: no box (h is read with bounds checks): at p = 7 its 24 KB buy a fourth slab per phase instead
     static constexpr bool A_IN_SMEM = (P < 11);
     static constexpr int SB = S::dh + 9;       // box side: 4 zeros below, 4 above
