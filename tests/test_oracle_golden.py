@@ -120,7 +120,7 @@ def test_factorised_identities_match_reference_intermediates():
             assert int(M[r, c]) == want
 
 
-@pytest.mark.parametrize("name", ["r1_spectrum_p5.txt", "r1_spectrum_p7.txt", "r1f_spectrum_p7_matrix_free.txt"])
+@pytest.mark.parametrize("name", ["r1_spectrum_p5.txt", "r1_spectrum_p7.txt", "r1j_spectrum_p7.txt", "r1f_spectrum_p7_matrix_free.txt"])
 def test_spectrum_witnesses(name):
     """The witnesses the GPU spectrum searches wrote (profiles/, fixture-table rows `p ; height ; poly`: one surface for
     every height 1..10 and infinity over F_5 and F_7) recomputed by the CPU oracle."""
