@@ -235,8 +235,8 @@ k_delta(const uint8_t* __restrict__ h_all, const uint8_t* __restrict__ A_all, co
             }
             __syncthreads();
         }
-        for (int rho1_0 = 0; rho1_0 < P; rho1_0 += C::KS) {
-        const int ks = min(C::KS, P - rho1_0);
+        int ks_step = C::KS;
+        for (int rho1_0 = 0; rho1_0 < P; rho1_0 += ks_step) {
         const int I1_0 = I1 + rho1_0;
         const int goff = S::gbase(I1_0, 0);
         // bytes of the phase's slabs with their guards; in the last layer (I1_0 = D) only the first slab exists.
@@ -244,6 +244,14 @@ k_delta(const uint8_t* __restrict__ h_all, const uint8_t* __restrict__ A_all, co
         const int sl_a = S::D - I1_0 + 1, sl_b = S::D - I1_0 + 2 + 2 * S::G;
         const int sl_ab = sl_a * sl_b, sl_apb = sl_a + sl_b;
         auto slabs_before = [&](int k) { return (k * sl_ab - sl_apb * ((k * (k - 1)) >> 1) + ((k - 1) * k * (2 * k - 1)) / 6) >> 1; };
+        // As many consecutive slabs as the phase buffer holds (it is sized for the KS largest ones, layer 0): the smaller slabs
+        // of the later layers go through in fewer phases, i.e. fewer cluster barriers (p = 7: 49 -> 32 phases; p = 11: 441 -> 215).
+        int ks = min(C::KS, P - rho1_0);
+        if constexpr (C::KS < P) {
+            const int kmax = min(P - rho1_0, S::D - I1_0 + 1);  // slabs that exist
+            while (ks < kmax && slabs_before(ks + 1) <= C::slabs_bytes(C::KS)) ++ks;
+        }
+        ks_step = ks;
         const int bytes = slabs_before(max(0, min(ks, S::D - I1_0 + 1)));
         if (bytes == 0) continue;  // uniform over the cluster: no slab, nothing to compute or flush
         uint8_t* slab0 = sSlab + (goff & 15);  // sSlab[0] <-> Delta offset goff & ~15
