@@ -58,7 +58,7 @@ struct DeltaCfg {
 #define QFS_DELTA_NT11 512
 #endif
 #ifndef QFS_DELTA_NT7
-#define QFS_DELTA_NT7 512
+#define QFS_DELTA_NT7 256
 #endif
 #ifndef QFS_DELTA_NT5
 #define QFS_DELTA_NT5 256
@@ -73,7 +73,10 @@ struct DeltaCfg {
     static constexpr int TMAX = (S::d + 1) * (S::d + 2) / 2;  // points (s2,s3) of the layer s1 = 0
     static constexpr int TPAD = (TMAX + 31) & ~31;
     static constexpr int RBH = (S::dh + 1) * (S::dh + 1);     // row bases of basis(dh) (bounds-checked path)
-    static constexpr int KS = (P >= 11) ? 1 : (P >= 7 ? 4 : P);  // slabs (consecutive rho1 of one layer) per phase; p = 7: 4+3 per layer (was 3+3+1: F_7 19.6 -> 18.0 ms)
+#ifndef QFS_DELTA_KS7
+#define QFS_DELTA_KS7 1
+#endif
+    static constexpr int KS = (P >= 11) ? 1 : (P >= 7 ? QFS_DELTA_KS7 : P);  // slabs (consecutive rho1 of one layer) the phase buffer is sized for (layer 0); p = 7: one slab (48 KB of shared memory, four 256-thread CTAs per SM: 17.1 -> 16.0 ms against four slabs and two 512-thread CTAs)
     static QFS_HD constexpr int slab_bytes(int I1) { return qc2(S::D - I1 + 2) + S::G * (S::D - I1 + 1); }
     static QFS_HD constexpr int slabs_bytes(int n) { int t = 0; for (int k = 0; k < n; ++k) t += slab_bytes(k); return t; }
     static constexpr int SLAB = slabs_bytes(KS) + 32;
@@ -245,7 +248,7 @@ k_delta(const uint8_t* __restrict__ h_all, const uint8_t* __restrict__ A_all, co
         const int sl_ab = sl_a * sl_b, sl_apb = sl_a + sl_b;
         auto slabs_before = [&](int k) { return (k * sl_ab - sl_apb * ((k * (k - 1)) >> 1) + ((k - 1) * k * (2 * k - 1)) / 6) >> 1; };
         // As many consecutive slabs as the phase buffer holds (it is sized for the KS largest ones, layer 0): the smaller slabs
-        // of the later layers go through in fewer phases, i.e. fewer cluster barriers (p = 7: 49 -> 32 phases; p = 11: 441 -> 215).
+        // of the later layers go through in fewer phases, i.e. fewer cluster barriers (p = 11: 441 -> 215 phases).
         int ks = min(C::KS, P - rho1_0);
         if constexpr (C::KS < P) {
             const int kmax = min(P - rho1_0, S::D - I1_0 + 1);  // slabs that exist
