@@ -11,7 +11,7 @@ def _line(name):
 
 
 def test_gpu_arm_line_has_the_contract_keys():
-    d = _line("r1k_bench_line.json")
+    d = _line("r1l_bench_line.json")
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
               "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks"):
         assert k in d, k
@@ -37,7 +37,7 @@ def test_gpu_arm_line_has_the_contract_keys():
 
 
 def test_reference_arm_line():
-    d = _line("r1k_bench_reference_arm.json")
+    d = _line("r1l_bench_reference_arm.json")
     assert d["impl"] == "reference" and d["unit"] == "surfaces/s" and d["gpu_launches"] == 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["e2e"]["value"] == d["value"] == d["cpu_baseline"]["value"] and d["cpu_baseline"]["kind"] == "port"
