@@ -142,3 +142,63 @@ def test_bound_semantics(bound):
     hs, its = _engine(p).heights(coeffs, bound)
     ohs, oits = oracle.heights_batch(coeffs, p, bound)
     assert np.array_equal(hs, ohs) and np.array_equal(its, oits)
+
+
+# ---- F_11: the reference's own intermediates (tests/golden/make_golden_p11.py; ~5 CPU-minutes per surface) ----------------
+def _p11():
+    z = np.load(os.path.join(GOLDEN, "stages_p11.npz"))
+    return z, int(z["count"])
+
+
+def test_f11_stage_power_golden():
+    z, n = _p11()
+    coeffs = np.stack([z[f"s{i}_coeffs"] for i in range(n)])
+    g, fed = _engine(11).stage_power(coeffs)
+    for i in range(n):
+        assert np.array_equal(g[i], z[f"s{i}_g"]), f"g mismatch surface {i}"
+        assert not fed[i]
+
+
+def test_f11_delta_matrix_chain_golden():
+    """Delta (sha256 of the dense 14 391 741-entry vector + every 997th entry), M (sha256 of the 12341 x 12341 operator + five
+    rows) and the whole matvec trace, heights and iteration counts of eight F_11 surfaces against what the reference
+    computed (extended suite of the reference, tests/test_acceptance.py:84-89; tests/test_mtsmatrix.py:174-198)."""
+    z, n = _p11()
+    eng = _engine(11)
+    coeffs = np.stack([z[f"s{i}_coeffs"] for i in range(n)])
+    for lo in range(0, n, 2):        # two surfaces at a time: 2 x 152 MB of M on the host
+        sel = list(range(lo, min(n, lo + 2)))
+        dl = eng.stage_delta(coeffs[sel])
+        for k, i in enumerate(sel):
+            assert np.array_equal(dl[k][::997], z[f"s{i}_delta_every"]), f"Delta sample mismatch surface {i}"
+            assert int(np.count_nonzero(dl[k])) == int(z[f"s{i}_delta_nnz"])
+            assert hashlib.sha256(dl[k].tobytes()).digest() == bytes(z[f"s{i}_delta_sha"]), f"Delta sha256 mismatch surface {i}"
+        M = eng.stage_matrix(dl)
+        g = np.stack([z[f"s{i}_g"] for i in sel])
+        for k, i in enumerate(sel):
+            assert np.array_equal(M[k][z[f"s{i}_M_rows_idx"]], z[f"s{i}_M_rows"]), f"M rows mismatch surface {i}"
+            assert hashlib.sha256(np.ascontiguousarray(M[k]).tobytes()).digest() == bytes(z[f"s{i}_M_sha"]), f"M sha256 mismatch surface {i}"
+        hs, its, tr = eng.stage_matvec_chain(M, g, 9, trace=True)
+        for k, i in enumerate(sel):
+            assert int(hs[k]) == int(z[f"s{i}_height"]) and int(its[k]) == int(z[f"s{i}_iters"])
+            assert np.array_equal(tr[k][: its[k]], z[f"s{i}_trace"]), f"trace mismatch surface {i}"
+        del M, dl
+    hs, its = eng.heights(coeffs, 10)
+    assert [int(h) for h in hs] == [int(z[f"s{i}_height"]) for i in range(n)]
+    assert [int(t) for t in its] == [int(z[f"s{i}_iters"]) for i in range(n)]
+
+
+def test_f7_chain_trace_golden():
+    """F_7: build M on the GPU from the golden Delta, check its sha256, then every intermediate vector of the matvec chain
+    against the reference's trace (the golden file holds only five rows of each 2925 x 2925 matrix)."""
+    z, n = _stages(7)
+    idx = [i for i in range(n) if f"s{i}_delta" in z.files]
+    eng = _engine(7)
+    M = eng.stage_matrix(np.stack([z[f"s{i}_delta"] for i in idx]))
+    for k, i in enumerate(idx):
+        assert hashlib.sha256(np.ascontiguousarray(M[k]).tobytes()).digest() == bytes(z[f"s{i}_Msha"])
+    g = np.stack([z[f"s{i}_g"] for i in idx])
+    hs, its, tr = eng.stage_matvec_chain(M, g, 9, trace=True)
+    for k, i in enumerate(idx):
+        assert int(hs[k]) == int(z[f"s{i}_height"]) and int(its[k]) == int(z[f"s{i}_iters"])
+        assert np.array_equal(tr[k][: its[k]], z[f"s{i}_trace"]), f"trace mismatch surface {i}"
