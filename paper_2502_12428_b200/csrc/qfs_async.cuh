@@ -42,6 +42,21 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity)
         "r"(parity)
         : "memory");
 }
+// the same for a thread that expects to wait long: the hardware may suspend it for up to the hint (ns) per try
+__device__ __forceinline__ void mbar_wait_backoff(uint32_t bar, uint32_t parity)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAITB_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        "@p bra DONEB_%=;\n"
+        "bra WAITB_%=;\n"
+        "DONEB_%=:\n"
+        "}\n" ::"r"(bar),
+        "r"(parity), "r"(20000u)
+        : "memory");
+}
 __device__ __forceinline__ void mbar_arrive(uint32_t bar)
 {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");

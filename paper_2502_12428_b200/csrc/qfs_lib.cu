@@ -84,7 +84,7 @@ struct qfs_ctx {
     int staged_multi = 0;
     int delta_direct = 0;                           // QFS_DELTA_DIRECT: use k_delta_direct for every prime (cross-check)
     int delta_version = 2;                          // QFS_DELTA_V: 2 = tensor-core kernel (k_delta_mma), 1 = DP4A slab kernel (k_delta)
-    DevBuf ecm, dphases, dpieces, dparts;           // k_delta_mma: class-major coefficient tables (chunk-sized), phase plan
+    DevBuf ecm, hbox, dphases, dpieces, dparts;     // k_delta_mma: class-major coefficient tables and interleaved h boxes (chunk-sized), phase plan
     int matrix_version = 6;                         // 6 = shared-memory staged builder, 4 = direct gather (QFS_MATRIX_V)
     int* h_flags = nullptr;                         // pinned mirror of flags
 };
@@ -287,6 +287,7 @@ int build_tables(qfs_ctx* ctx)
         CU(cudaMemcpy(ctx->dpieces.ptr, plan.pieces.data(), plan.pieces.size() * sizeof(DeltaPiece), cudaMemcpyHostToDevice));
         CU(cudaMemcpy(ctx->dparts.ptr, plan.parts.data(), plan.parts.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
         CU(cudaFuncSetAttribute(k_delta_mma<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, DeltaMmaCfg<P>::SMEM));
+        CU(cudaFuncSetAttribute(k_delta_box<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * Shape<P>::Nh_pad));
     }
     if constexpr (DeltaCfg<P>::SMEM <= 227 * 1024) {
         // resident 4-CTA clusters (a GPC whose SM count is not a multiple of what a cluster needs leaves SMs idle)
@@ -315,7 +316,7 @@ template <int P>
 size_t per_surface_bytes()
 {
     using S = Shape<P>;
-    return (size_t)S::N * S::pitch + S::Lg_pad + 3 * (size_t)S::pitch + S::Nh_pad + S::NE_pad + DeltaMmaCfg<P>::EC_STRIDE;
+    return (size_t)S::N * S::pitch + S::Lg_pad + 3 * (size_t)S::pitch + S::Nh_pad + S::NE_pad + DeltaMmaCfg<P>::EC_STRIDE + DeltaMmaCfg<P>::HBOX_WORDS;
 }
 
 template <int P>
@@ -329,6 +330,7 @@ int reserve_chunk(qfs_ctx* ctx, size_t cap)
     CU(ctx->E.reserve(cap * S::NE_pad));
     CU(ctx->delta.reserve(cap * (size_t)S::Lg_pad));
     CU(ctx->ecm.reserve(cap * (size_t)DeltaMmaCfg<P>::EC_STRIDE));
+    CU(ctx->hbox.reserve(cap * DeltaMmaCfg<P>::HBOX_WORDS));
     CU(ctx->M.reserve(cap * (size_t)S::N * S::pitch));
     CU(ctx->v1.reserve(cap * S::pitch));
     return QFS_OK;
@@ -366,14 +368,17 @@ int launch_delta(qfs_ctx* ctx, int count)
     if (ctx->delta_version == 2 && !ctx->delta_direct) {
         // tensor-core kernel: class-major coefficient tables, then one CTA per (quad, part of the phase plan)
         using DM = DeltaMmaCfg<P>;
-        CU(ctx->ecm.reserve((size_t)count * DM::EC_STRIDE));
-        const dim3 pgrid((unsigned)((P * P * P + 127) / 128), (unsigned)count);
-        k_delta_prep<P><<<pgrid, 128, 0, ctx->stream>>>(ctx->E.as<uint8_t>(), ctx->ecm.as<uint8_t>(), count);
-        ctx->stats.kernel_launches++;
-        CU(cudaGetLastError());
         const unsigned quads = (unsigned)((count + 3) / 4);
+        CU(ctx->ecm.reserve((size_t)count * DM::EC_STRIDE));
+        CU(ctx->hbox.reserve((size_t)quads * DM::HBOX_WORDS * 4));
+        k_delta_prep<P><<<(unsigned)count, 128, S::NE_pad, ctx->stream>>>(ctx->E.as<uint8_t>(), ctx->ecm.as<uint8_t>(), count);
+        k_delta_box<P><<<quads, 256, 4 * S::Nh_pad, ctx->stream>>>(ctx->h.as<uint8_t>(), ctx->A.as<uint8_t>(), ctx->ecm.as<uint8_t>(),
+                                                                  ctx->unrank.as<uint32_t>() + qunrank_offset(P - 1),
+                                                                  ctx->hbox.as<uint32_t>(), count);
+        ctx->stats.kernel_launches += 2;
+        CU(cudaGetLastError());
         k_delta_mma<P><<<quads * DM::SPLIT, DM::NT, DM::SMEM, ctx->stream>>>(
-            ctx->h.as<uint8_t>(), ctx->A.as<uint8_t>(), ctx->ecm.as<uint8_t>(), ctx->dphases.as<DeltaPhase>(),
+            ctx->hbox.as<uint32_t>(), ctx->A.as<uint8_t>(), ctx->ecm.as<uint8_t>(), ctx->dphases.as<DeltaPhase>(),
             ctx->dpieces.as<DeltaPiece>(), ctx->dparts.as<uint32_t>(), ctx->delta.as<uint8_t>(), count);
         ctx->stats.kernel_launches++;
         CU(cudaGetLastError());
@@ -573,7 +578,7 @@ int run_heights(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, int bound, int8_t
             if (!ctx->auto_limit) {  // asked once per context: cudaMemGetInfo costs milliseconds on a busy heap
                 size_t fr = 0, tot = 0;
                 CU(cudaMemGetInfo(&fr, &tot));
-                size_t held = ctx->g.cap + ctx->A.cap + ctx->h.cap + ctx->E.cap + ctx->delta.cap + ctx->M.cap + ctx->v1.cap + ctx->ecm.cap;
+                size_t held = ctx->g.cap + ctx->A.cap + ctx->h.cap + ctx->E.cap + ctx->delta.cap + ctx->M.cap + ctx->v1.cap + ctx->ecm.cap + ctx->hbox.cap;
                 ctx->auto_limit = (size_t)((double)(fr + held) * 0.4);
             }
             limit = ctx->auto_limit;
@@ -860,7 +865,7 @@ void qfs_destroy(qfs_ctx* ctx)
     cudaSetDevice(ctx->device);
     DevBuf* bufs[] = {&ctx->flags, &ctx->colinfo, &ctx->groups, &ctx->runs, &ctx->unrank, &ctx->coeffs, &ctx->heights, &ctx->iters, &ctx->list,
                       &ctx->g, &ctx->h, &ctx->A, &ctx->E, &ctx->delta, &ctx->M, &ctx->v1, &ctx->tapA, &ctx->tapB, &ctx->items, &ctx->vacc, &ctx->chain_scratch,
-                      &ctx->ecm, &ctx->dphases, &ctx->dpieces, &ctx->dparts};
+                      &ctx->ecm, &ctx->hbox, &ctx->dphases, &ctx->dpieces, &ctx->dparts};
     for (DevBuf* b : bufs) b->release();
     for (auto& e : ctx->ev) if (e) cudaEventDestroy(e);
     for (auto& e : ctx->ev_total) if (e) cudaEventDestroy(e);
@@ -1033,7 +1038,7 @@ int qfs_debug_fill_workspaces(qfs_ctx* ctx, int byte)
     if (!ctx) return QFS_EINVAL;
     CU(cudaSetDevice(ctx->device));
     DevBuf* bufs[] = {&ctx->g, &ctx->h, &ctx->A, &ctx->E, &ctx->delta, &ctx->M, &ctx->v1, &ctx->vacc, &ctx->tapA, &ctx->tapB,
-                      &ctx->coeffs, &ctx->heights, &ctx->iters, &ctx->list, &ctx->chain_scratch, &ctx->ecm};
+                      &ctx->coeffs, &ctx->heights, &ctx->iters, &ctx->list, &ctx->chain_scratch, &ctx->ecm, &ctx->hbox};
     for (DevBuf* b : bufs)
         if (b->ptr) CU(cudaMemsetAsync(b->ptr, byte, b->cap, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));

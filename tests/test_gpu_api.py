@@ -48,7 +48,7 @@ def test_f11_published_rows():
 
 def test_f13_published_rows():
     """The five F_13 rows of the published table (k3_tables.txt:30-34): 20825 x 20825 operator, 434 MB per surface,
-    Delta from k_delta_direct (the slab kernel does not fit shared memory at p = 13)."""
+    Delta from k_delta_mma (SPLIT CTAs per quad)."""
     import paper_2502_12428_b200 as q
     rows = [r for r in ROWS if r["p"] == 13]
     hs, its = q.height_batch(13, np.array([r["coeffs"] for r in rows], dtype=np.uint8))
@@ -60,25 +60,29 @@ def test_f13_published_rows():
     assert set(int(h) for h in hs) <= {1, 2, 3} and (hs == 1).sum() >= 30
 
 
-@pytest.mark.parametrize("p", [3, 5, 7, 11])
-def test_direct_witt_carry_kernel_equals_the_slab_kernel(p, monkeypatch):
-    """k_delta_direct (the p = 13 path) against k_delta on primes that have both: identical dense Delta and,
-    through the whole pipeline, identical heights."""
+@pytest.mark.parametrize("p", [3, 5, 7, 11, 13])
+def test_the_three_witt_carry_kernels_agree(p, monkeypatch):
+    """k_delta_mma (tensor cores, the default) against the two DP4A kernels it replaced -- k_delta (slabs, 4-CTA clusters; does not
+    fit shared memory at p = 13) and k_delta_direct -- on the same surfaces: identical dense Delta and, through the whole pipeline,
+    identical heights (mirrors the reference pinning its three matrix builders on each other, tests/test_acceptance.py:110-125)."""
     import paper_2502_12428_b200 as q
     from paper_2502_12428_b200.engine import Engine, get_engine
     c = q.sample_block(p, 6 if p < 11 else 2, 21, 0)
+    big = q.sample_block(p, 300 if p < 11 else 30, 22, 0)
     want = get_engine(p, 0).stage_delta(c)
-    monkeypatch.setenv("QFS_DELTA_DIRECT", "1")
-    eng = Engine(p, 0)
-    try:
-        got = eng.stage_delta(c)
-        assert np.array_equal(got, want)
-        big = q.sample_block(p, 300 if p < 11 else 30, 22, 0)
-        h1, i1 = eng.heights(big, 10)
-        h0, i0 = get_engine(p, 0).heights(big, 10)
-        assert np.array_equal(h1, h0) and np.array_equal(i1, i0)
-    finally:
-        eng.close()
+    h0, i0 = get_engine(p, 0).heights(big, 10)
+    for var, val in (("QFS_DELTA_DIRECT", "1"), ("QFS_DELTA_V", "1")):
+        if p == 13 and var == "QFS_DELTA_V":
+            continue
+        monkeypatch.setenv(var, val)
+        eng = Engine(p, 0)
+        try:
+            assert np.array_equal(eng.stage_delta(c), want), var
+            h1, i1 = eng.heights(big, 10)
+            assert np.array_equal(h1, h0) and np.array_equal(i1, i0), var
+        finally:
+            eng.close()
+            monkeypatch.delenv(var)
 
 
 @pytest.mark.parametrize("p", [3, 5, 7, 11])
@@ -201,7 +205,7 @@ def test_full_size_f7_batch_matrix_path_equals_matrix_free_iteration():
     assert np.array_equal(its[:10000].astype(np.int64), z["iters"].astype(np.int64))
 
 
-@pytest.mark.parametrize("p", [3, 5, 7])
+@pytest.mark.parametrize("p", [3, 5, 7, 11])
 def test_results_do_not_depend_on_what_the_workspaces_held(p):
     """Recycled device memory is not zero: poison every workspace between calls (qfs_debug_fill_workspaces)
     and demand identical heights, stage taps and exports.  Regression: the last slab of Delta (I1 = D) and its
@@ -213,6 +217,8 @@ def test_results_do_not_depend_on_what_the_workspaces_held(p):
     coeffs = np.array([r["coeffs"] for r in rows], dtype=np.uint8) if rows else q.sample_block(3, 40, 4, 0)
     coeffs = np.concatenate([coeffs, q.sample_block(p, 37, 9, 1)])
     want_h, want_i = eng.heights(coeffs, 10)
+    if rows:
+        assert [int(h) for h in want_h[:len(rows)]] == [int(r["height"]) for r in rows]   # 0 = infinity in both
     want_d = eng.stage_delta(coeffs[:3])
     want_m = eng.export_matrix(coeffs[:2])
     for byte in (0xFF, 0x01, 0xA7):
@@ -223,9 +229,6 @@ def test_results_do_not_depend_on_what_the_workspaces_held(p):
         assert np.array_equal(eng.stage_delta(coeffs[:3]), want_d)
         eng.debug_fill_workspaces(byte)
         assert np.array_equal(eng.export_matrix(coeffs[:2]), want_m)
-    if rows:
-        assert [int(h) for h in want_h[:len(rows)]] == [0 if r["height"] in ("inf", None) or r["height"] == 0 else int(r["height"]) for r in rows] \
-            or True  # heights of the published rows are pinned in test_verify_fixtures_on_gpu
 
 
 def test_matrix_free_iteration_equals_the_reference_heights():

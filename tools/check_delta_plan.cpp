@@ -22,7 +22,7 @@ int check()
     if (!delta_plan<P>(plan)) { printf("p=%d: plan failed (SBW/MPTS too small)\n", P); return 1; }
     const int Lend = (S::Lg + 3) & ~3;
     std::vector<uint8_t> stored(Lend, 0), entry(Lend, 0);
-    long tiles = 0, pts = 0, words = 0;
+    long tiles = 0, pts = 0, words = 0, blocks = 0;
     int errors = 0;
     auto bad = [&](const char* what, int a, int b, int c) {
         if (errors++ < 10) printf("p=%d: %s (%d %d %d)\n", P, what, a, b, c);
@@ -30,8 +30,10 @@ int check()
     for (size_t ip = 0; ip < plan.phases.size(); ++ip) {
         const DeltaPhase& ph = plan.phases[ip];
         const int s1 = ph.s1, ns = S::d - s1, n0 = S::D - P * s1 - ph.rho1a;
-        if (ph.nwords > (uint32_t)C::SBW || ph.npts > C::MPTS) bad("phase exceeds the buffers", (int)ip, (int)ph.nwords, ph.npts);
+        if (ph.nwords > (uint32_t)C::SBW) bad("phase exceeds the staging buffer", (int)ip, (int)ph.nwords, ph.npts);
+        std::vector<uint8_t> cover(ph.nwords, 0);   // every staged word: one entry or one zero of a guard item
         tiles += (ph.npts + 15) / 16;
+        blocks += (ph.flags & DPH_BLOCK) ? 1 : 0;
         pts += ph.npts;
         words += ph.nwords;
         uint32_t po = 0;
@@ -69,8 +71,26 @@ int check()
                 const int e = (int)pc.ga + (w - (int)pc.po);
                 if (e != S::gbase(I1, I2) + I4) { bad("word is not the entry's offset", I1, I2, e - (S::gbase(I1, I2) + I4)); continue; }
                 if (entry[e]++) bad("exponent produced twice", I1, I2, I3);
+                cover[w]++;
             }
         }
+        // the kernel's guard items
+        const int ns2 = ph.s2b - ph.s2a;
+        for (int gi = 0; gi < ph.nrho1 * P * ns2; ++gi) {
+            const int k = gi / (P * ns2), j = gi - k * (P * ns2);
+            const int I2 = P * ph.s2a + j, nk = n0 - k;
+            const DeltaPiece& pc = plan.pieces[ph.piece0 + k];
+            if (!(I2 <= nk && pc.nw > 0)) continue;
+            const int rs = delta_run_start<P>(nk, I2, pc.cconst, (int)pc.po);
+            for (int w = (j == 0 ? 0 : rs - S::G); w < rs; ++w) {
+                if (w < 0 || w >= (int)pc.nw) { bad("guard word outside the piece", (int)ip, k, w); break; }
+                cover[pc.po + w]++;
+            }
+            if (I2 == std::min(P * ph.s2b - 1, nk))
+                for (int w = rs + (nk - I2 + 1); w < (int)pc.nw; ++w) cover[pc.po + w]++;
+        }
+        for (uint32_t w = 0; w < ph.nwords; ++w)
+            if (cover[w] != 1) { bad("staged word not written exactly once", (int)ip, (int)w, cover[w]); break; }
     }
     for (int e = 0; e < Lend; ++e)
         if (stored[e] != 1) { bad("entry not stored", e, stored[e], 0); break; }
@@ -84,9 +104,9 @@ int check()
     for (int i = 0; i < C::SPLIT; ++i)
         if (plan.parts[i] > plan.parts[i + 1]) bad("parts not monotone", i, 0, 0);
     if (plan.parts[0] != 0 || plan.parts[C::SPLIT] != plan.phases.size()) bad("parts do not cover the phases", 0, 0, 0);
-    printf("p=%d: %zu phases, %zu pieces, %ld points in %ld tiles (%.1f%% of the tile rows), classes %d of %d, %ld staged words "
+    printf("p=%d: %zu phases in %ld blocks, %zu pieces, %ld points in %ld tiles (%.1f%% of the tile rows), classes %d of %d, %ld staged words "
            "(%.2f x L), smem %d bytes: %s\n",
-           P, plan.phases.size(), plan.pieces.size(), pts, tiles, 100.0 * pts / (16.0 * tiles), C::NCLS, C::NCLS_PAD, words,
+           P, plan.phases.size(), blocks, plan.pieces.size(), pts, tiles, 100.0 * pts / (16.0 * tiles), C::NCLS, C::NCLS_PAD, words,
            (double)words / S::L, C::SMEM, errors ? "FAILED" : "ok");
     return errors;
 }
