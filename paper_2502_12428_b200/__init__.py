@@ -12,6 +12,7 @@ from .height import (INFINITE, HeightResult, SurfaceProblem, default_bound, heig
 from .mtsmatrix import (MtsMatrix, build_mts, build_mts_batch, matrix_from_bytes, matrix_from_text, matrix_to_bytes,
                         matrix_to_text, target_degree)
 from .quartic import Quartic, coeff_vector, parse_poly, poly_to_text
+from .stages import DenseForm, DenseVector, delta1, fedder_survives, matvec, power_mod_p, to_dense
 from .search import (FixtureRow, FixtureVerdict, FoundSurface, HeightHistogram, SearchConfig, found_surfaces_text,
                      histogram_text, parse_fixtures, run_search, sample_block, sample_surface, spectrum_rows,
                      spectrum_search, verify_fixtures)
@@ -34,4 +35,5 @@ __all__ = [
     "spectrum_search", "verify_fixtures", "fixtures_path",
     "Cubic", "cubic_height_batch", "MtsMatrix", "build_mts", "build_mts_batch", "matrix_from_bytes", "matrix_from_text", "matrix_to_bytes",
     "matrix_to_text", "target_degree",
+    "DenseForm", "DenseVector", "delta1", "fedder_survives", "matvec", "power_mod_p", "to_dense",
 ]

@@ -25,7 +25,7 @@
 
 namespace {
 
-std::string g_create_error;
+thread_local std::string g_create_error;   // errors of the context-free entries (qfs_create, qfs_cubic_heights), per calling thread
 
 struct DevBuf {
     void* ptr = nullptr;
@@ -51,6 +51,21 @@ struct DevBuf {
 
 enum { EV_COUNT = 8 };
 
+// Every entry point runs on its context's device and leaves the caller's current device as it found it.
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev)
+    {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) cudaSetDevice(dev);
+        else prev = -1;
+    }
+    ~DeviceGuard()
+    {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
 }  // namespace
 
 struct qfs_ctx {
@@ -60,6 +75,7 @@ struct qfs_ctx {
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[EV_COUNT] = {};
     cudaEvent_t ev_total[2] = {};
+    std::vector<cudaEvent_t> chunk_ev;              // five per chunk of a call: stage boundaries, read after the call's last sync
     size_t workspace_limit = 0;
     size_t auto_limit = 0;                          // default workspace budget, fixed at first use
     size_t chunk_override = 0;
@@ -162,6 +178,15 @@ __global__ void k_widen_u16(const uint8_t* __restrict__ M, int n, int pitch, uin
     const uint8_t* src = M + (size_t)blockIdx.y * n * pitch + (size_t)r * pitch;
     uint16_t* dst = out + ((size_t)blockIdx.y * n + r) * n;
     for (int c = threadIdx.x; c < n; c += blockDim.x) dst[c] = src[c];
+}
+
+// total number of operator applications of a call (stats.matvec_steps), also when the outputs stay on the device
+__global__ void __launch_bounds__(1024) k_sum_iters(const int8_t* __restrict__ iters, size_t B, int* __restrict__ total)
+{
+    int s = 0;
+    for (size_t i = (size_t)blockIdx.x * 1024 + threadIdx.x; i < B; i += (size_t)gridDim.x * 1024) s += iters[i];
+    s = __reduce_add_sync(0xffffffffu, s);
+    if ((threadIdx.x & 31) == 0 && s) atomicAdd(total, s);
 }
 
 // heights[i] == -1 (pending) -> 0 (infinity); used when bound < 2 (height.py:126-127)
@@ -525,12 +550,15 @@ int run_heights(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, int bound, int8_t
     ctx->stats.surfaces = (int64_t)B;
     if (B == 0) return QFS_OK;
     if (B > 0x7fffffffULL) return fail(ctx, QFS_EINVAL, "batch too large");
-    CU(cudaSetDevice(ctx->device));
-    if (user_stream) {
-        CU(cudaEventRecord(ctx->ev[0], (cudaStream_t)user_stream));
+    DeviceGuard guard_(ctx->device);
+    const bool in_dev = is_device_ptr(coeffs), hout_dev = is_device_ptr(heights), iout_dev = is_device_ptr(iters);
+    if (user_stream || in_dev || hout_dev || iout_dev) {
+        // Order the pipeline after whatever the caller has queued: on the stream it names, or -- no stream named -- on the
+        // legacy default stream, which is where an unsuspecting producer of a device buffer runs (ctx->stream is non-blocking
+        // and would not wait for it by itself).
+        CU(cudaEventRecord(ctx->ev[0], user_stream ? (cudaStream_t)user_stream : cudaStreamLegacy));
         CU(cudaStreamWaitEvent(ctx->stream, ctx->ev[0], 0));
     }
-    const bool in_dev = is_device_ptr(coeffs), hout_dev = is_device_ptr(heights), iout_dev = is_device_ptr(iters);
     const uint8_t* d_coeffs = coeffs;
     if (!in_dev) {
         CU(ctx->coeffs.reserve(B * 35));
@@ -579,7 +607,7 @@ int run_heights(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, int bound, int8_t
                 size_t fr = 0, tot = 0;
                 CU(cudaMemGetInfo(&fr, &tot));
                 size_t held = ctx->g.cap + ctx->A.cap + ctx->h.cap + ctx->E.cap + ctx->delta.cap + ctx->M.cap + ctx->v1.cap + ctx->ecm.cap + ctx->hbox.cap;
-                ctx->auto_limit = (size_t)((double)(fr + held) * 0.4);
+                ctx->auto_limit = (size_t)((double)(fr + held) * 0.75);
             }
             limit = ctx->auto_limit;
         }
@@ -601,16 +629,26 @@ int run_heights(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, int bound, int8_t
         }
         ctx->stats.chunk_capacity = (int64_t)cap;
         const uint32_t* d_list = ctx->list.as<uint32_t>();
-        for (size_t done = 0; done < (size_t)hard; done += cap) {
+        // Chunks are queued back to back: the stage boundaries of every chunk get their own events, read after the one
+        // synchronisation at the end of the call (no host round trip between chunks).
+        const size_t nchunks = ((size_t)hard + cap - 1) / cap;
+        while (ctx->chunk_ev.size() < 5 * nchunks) {
+            cudaEvent_t e = nullptr;
+            CU(cudaEventCreate(&e));
+            ctx->chunk_ev.push_back(e);
+        }
+        size_t ci = 0;
+        for (size_t done = 0; done < (size_t)hard; done += cap, ++ci) {
             const int cnt = (int)std::min<size_t>(cap, (size_t)hard - done);
+            cudaEvent_t* ev = &ctx->chunk_ev[5 * ci];
             int rc;
-            CU(cudaEventRecord(ctx->ev[0], ctx->stream));
+            CU(cudaEventRecord(ev[0], ctx->stream));
             if ((rc = launch_power_full<P>(ctx, d_coeffs, d_list + done, cnt, nullptr))) return rc;
-            CU(cudaEventRecord(ctx->ev[1], ctx->stream));
+            CU(cudaEventRecord(ev[1], ctx->stream));
             if (matrix_free) {
                 // the operator iteration without Delta and without M (qfs_free.cuh): stage times delta = matrix = 0
-                CU(cudaEventRecord(ctx->ev[2], ctx->stream));
-                CU(cudaEventRecord(ctx->ev[3], ctx->stream));
+                CU(cudaEventRecord(ev[2], ctx->stream));
+                CU(cudaEventRecord(ev[3], ctx->stream));
                 k_free<P><<<cnt, FreeCfg<P>::NT, FreeCfg<P>::SMEM, ctx->stream>>>(
                     ctx->g.as<uint8_t>(), ctx->h.as<uint8_t>(), ctx->E.as<uint8_t>(), ctx->unrank.as<uint32_t>() + qunrank_offset(P),
                     ctx->unrank.as<uint32_t>() + qunrank_offset(P - 1), d_list + done, bound - 1, d_heights, d_iters);
@@ -618,35 +656,32 @@ int run_heights(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, int bound, int8_t
                 CU(cudaGetLastError());
             } else {
                 if ((rc = launch_delta<P>(ctx, cnt))) return rc;
-                CU(cudaEventRecord(ctx->ev[2], ctx->stream));
+                CU(cudaEventRecord(ev[2], ctx->stream));
                 if ((rc = launch_matrix<P>(ctx, cnt, ctx->g.as<uint8_t>(), ctx->v1.as<uint8_t>()))) return rc;
-                CU(cudaEventRecord(ctx->ev[3], ctx->stream));
+                CU(cudaEventRecord(ev[3], ctx->stream));
                 if ((rc = launch_chain<P>(ctx, ctx->v1.as<uint8_t>(), d_list + done, cnt, 1, bound - 1, nullptr, d_heights, d_iters))) return rc;
             }
-            CU(cudaEventRecord(ctx->ev[4], ctx->stream));
-            CU(cudaEventSynchronize(ctx->ev[4]));
-            ctx->stats.ms_power += elapsed(ctx->ev[0], ctx->ev[1]);
-            ctx->stats.ms_delta += elapsed(ctx->ev[1], ctx->ev[2]);
-            ctx->stats.ms_matrix += elapsed(ctx->ev[2], ctx->ev[3]);
-            ctx->stats.ms_matvec += elapsed(ctx->ev[3], ctx->ev[4]);
+            CU(cudaEventRecord(ev[4], ctx->stream));
             ctx->stats.chunks++;
         }
-        int rc = check_device_flags(ctx);
+        k_sum_iters<<<(unsigned)std::min<size_t>((B + 1023) / 1024, 1024), 1024, 0, ctx->stream>>>(d_iters, B, d_flags + 3);
+        ctx->stats.kernel_launches++;
+        int rc = check_device_flags(ctx);   // the call's one synchronisation after the chunk loop
         if (rc) return rc;
+        ctx->stats.matvec_steps = ctx->h_flags[3];
+        for (size_t c = 0; c < nchunks; ++c) {
+            cudaEvent_t* ev = &ctx->chunk_ev[5 * c];
+            ctx->stats.ms_power += elapsed(ev[0], ev[1]);
+            ctx->stats.ms_delta += elapsed(ev[1], ev[2]);
+            ctx->stats.ms_matrix += elapsed(ev[2], ev[3]);
+            ctx->stats.ms_matvec += elapsed(ev[3], ev[4]);
+        }
     }
     CU(cudaEventRecord(ctx->ev_total[1], ctx->stream));
     if (!hout_dev) CU(cudaMemcpyAsync(heights, d_heights, B, cudaMemcpyDeviceToHost, ctx->stream));
     if (!iout_dev) CU(cudaMemcpyAsync(iters, d_iters, B, cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
     ctx->stats.ms_total = elapsed(ctx->ev_total[0], ctx->ev_total[1]);
-    if (hard > 0) {
-        // matvec steps: sum of iterations over hard surfaces (host outputs only; cheap)
-        if (!iout_dev) {
-            int64_t s = 0;
-            for (size_t i = 0; i < B; ++i) s += iters[i];
-            ctx->stats.matvec_steps = s;
-        }
-    }
     return QFS_OK;
 }
 
@@ -678,7 +713,7 @@ template <int P>
 int run_stage_power(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, uint8_t* g, uint8_t* fedder)
 {
     using S = Shape<P>;
-    CU(cudaSetDevice(ctx->device));
+    DeviceGuard guard_(ctx->device);
     CU(cudaMemsetAsync(ctx->flags.ptr, 0, 4 * sizeof(int), ctx->stream));
     const size_t slice = tap_slice<P>(ctx, B, per_surface_bytes<P>() - (size_t)S::N * S::pitch - S::Lg_pad + 64);
     CU(ctx->tapA.reserve(slice * 35));
@@ -703,7 +738,7 @@ template <int P>
 int run_stage_delta(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, uint8_t* delta)
 {
     using S = Shape<P>;
-    CU(cudaSetDevice(ctx->device));
+    DeviceGuard guard_(ctx->device);
     CU(cudaMemsetAsync(ctx->flags.ptr, 0, 4 * sizeof(int), ctx->stream));
     const size_t slice = tap_slice<P>(ctx, B, per_surface_bytes<P>() - (size_t)S::N * S::pitch + S::L);
     CU(ctx->tapA.reserve(slice * 35));
@@ -733,7 +768,7 @@ template <int P>
 int run_stage_matrix(qfs_ctx* ctx, const uint8_t* delta, size_t B, uint8_t* M)
 {
     using S = Shape<P>;
-    CU(cudaSetDevice(ctx->device));
+    DeviceGuard guard_(ctx->device);
     const size_t slice = tap_slice<P>(ctx, B, (size_t)S::N * S::pitch + (size_t)S::Lg_pad + S::L);
     for (size_t done = 0; done < B; done += slice) {
         const int cnt = (int)std::min(slice, B - done);
@@ -759,7 +794,7 @@ template <int P>
 int run_export_matrix(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, uint16_t* M16)
 {
     using S = Shape<P>;
-    CU(cudaSetDevice(ctx->device));
+    DeviceGuard guard_(ctx->device);
     CU(cudaMemsetAsync(ctx->flags.ptr, 0, 4 * sizeof(int), ctx->stream));
     const bool out_dev = is_device_ptr(M16);
     const size_t nn = (size_t)S::N * S::N;
@@ -788,7 +823,7 @@ int run_stage_chain(qfs_ctx* ctx, const uint8_t* M, const uint8_t* v0, size_t B,
                     int8_t* heights, int8_t* iters)
 {
     using S = Shape<P>;
-    CU(cudaSetDevice(ctx->device));
+    DeviceGuard guard_(ctx->device);
     if (max_steps < 0) return fail(ctx, QFS_EINVAL, "max_steps must be >= 0");
     const size_t slice = tap_slice<P>(ctx, B, (size_t)S::N * S::pitch + (size_t)(max_steps + 2) * S::pitch);
     CU(ctx->heights.reserve(B));
@@ -862,13 +897,14 @@ const char* qfs_last_error(const qfs_ctx* ctx) { return ctx ? ctx->error.c_str()
 void qfs_destroy(qfs_ctx* ctx)
 {
     if (!ctx) return;
-    cudaSetDevice(ctx->device);
+    DeviceGuard guard_(ctx->device);
     DevBuf* bufs[] = {&ctx->flags, &ctx->colinfo, &ctx->groups, &ctx->runs, &ctx->unrank, &ctx->coeffs, &ctx->heights, &ctx->iters, &ctx->list,
                       &ctx->g, &ctx->h, &ctx->A, &ctx->E, &ctx->delta, &ctx->M, &ctx->v1, &ctx->tapA, &ctx->tapB, &ctx->items, &ctx->vacc, &ctx->chain_scratch,
                       &ctx->ecm, &ctx->hbox, &ctx->dphases, &ctx->dpieces, &ctx->dparts};
     for (DevBuf* b : bufs) b->release();
     for (auto& e : ctx->ev) if (e) cudaEventDestroy(e);
     for (auto& e : ctx->ev_total) if (e) cudaEventDestroy(e);
+    for (auto& e : ctx->chunk_ev) if (e) cudaEventDestroy(e);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     if (ctx->h_flags) cudaFreeHost(ctx->h_flags);
     delete ctx;
@@ -991,7 +1027,7 @@ int qfs_cubic_heights(int device, int p, const uint8_t* coeffs, size_t B, int bo
     if (B == 0) return QFS_OK;
     if (!coeffs || !heights || !iters) return fail(ctx, QFS_EINVAL, "NULL buffer");
     if (B > 0x7fffffffULL) return fail(ctx, QFS_EINVAL, "batch too large");
-    CU(cudaSetDevice(device));
+    DeviceGuard guard_(device);
     const bool in_dev = is_device_ptr(coeffs), h_dev = is_device_ptr(heights), i_dev = is_device_ptr(iters);
     uint8_t* d_c = nullptr;
     int8_t *d_h = nullptr, *d_i = nullptr;
@@ -1036,7 +1072,7 @@ int qfs_cubic_heights(int device, int p, const uint8_t* coeffs, size_t B, int bo
 int qfs_debug_fill_workspaces(qfs_ctx* ctx, int byte)
 {
     if (!ctx) return QFS_EINVAL;
-    CU(cudaSetDevice(ctx->device));
+    DeviceGuard guard_(ctx->device);
     DevBuf* bufs[] = {&ctx->g, &ctx->h, &ctx->A, &ctx->E, &ctx->delta, &ctx->M, &ctx->v1, &ctx->vacc, &ctx->tapA, &ctx->tapB,
                       &ctx->coeffs, &ctx->heights, &ctx->iters, &ctx->list, &ctx->chain_scratch, &ctx->ecm, &ctx->hbox};
     for (DevBuf* b : bufs)

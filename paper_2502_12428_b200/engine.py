@@ -40,7 +40,8 @@ def _in_ptr(x, shape, what):
 
 
 class Engine:
-    """Owns one qfs_ctx.  Not thread-safe; use one Engine per GPU (get_engine caches them)."""
+    """Owns one qfs_ctx (single-threaded at the C ABI): every call into the library holds the engine's lock, so threads that
+    share an Engine (get_engine caches one per prime and GPU) take turns instead of running on the same workspaces."""
 
     def __init__(self, p, device=0, max_batch=0):
         self.lib = _native.load()
@@ -52,6 +53,11 @@ class Engine:
         if rc != 0:
             _native.raise_for(rc, self.lib.qfs_last_error(None).decode())
         self._h = handle
+        self._mutex = threading.RLock()
+
+    def _call(self, fn, *args):
+        with self._mutex:
+            self._check(fn(self._h, *args))
 
     def close(self):
         if getattr(self, "_h", None):
@@ -70,10 +76,10 @@ class Engine:
 
     # -- configuration -----------------------------------------------------------------------
     def set_workspace_limit(self, nbytes):
-        self._check(self.lib.qfs_set_workspace_limit(self._h, int(nbytes)))
+        self._call(self.lib.qfs_set_workspace_limit, int(nbytes))
 
     def set_chunk(self, n):
-        self._check(self.lib.qfs_set_chunk(self._h, int(n)))
+        self._call(self.lib.qfs_set_chunk, int(n))
 
     def stats(self):
         st = _native.QfsStats()
@@ -105,11 +111,15 @@ class Engine:
         hp = hs.data_ptr() if _is_torch(hs) else hs.ctypes.data
         ip = its.data_ptr() if _is_torch(its) else its.ctypes.data
         stream = None
-        if _is_torch(coeffs):
+        for t in (coeffs, hs, its):
+            if _is_torch(t) and t.is_cuda and t.device.index != self.device:
+                raise DomainError(f"tensor on {t.device} handed to the engine of cuda:{self.device}")
+        if _is_torch(coeffs) and coeffs.is_cuda:
             import torch
+            # the library orders its own stream behind this one (a NULL handle -- the default stream -- included)
             stream = torch.cuda.current_stream(coeffs.device).cuda_stream
         fn = self.lib.qfs_heights_free if matrix_free else self.lib.qfs_heights
-        self._check(fn(self._h, cptr, B, int(bound), hp, ip, stream))
+        self._call(fn, cptr, B, int(bound), hp, ip, stream)
         del keep
         return hs, its
 
@@ -119,14 +129,14 @@ class Engine:
         B = c.shape[0]
         g = np.empty((B, self.shape.N), dtype=np.uint8)
         fed = np.empty(B, dtype=np.uint8)
-        self._check(self.lib.qfs_stage_power(self._h, c.ctypes.data, B, g.ctypes.data, fed.ctypes.data))
+        self._call(self.lib.qfs_stage_power, c.ctypes.data, B, g.ctypes.data, fed.ctypes.data)
         return g, fed
 
     def stage_delta(self, coeffs):
         c = np.ascontiguousarray(coeffs, dtype=np.uint8).reshape(-1, 35)
         B = c.shape[0]
         out = np.empty((B, self.shape.L), dtype=np.uint8)
-        self._check(self.lib.qfs_stage_delta(self._h, c.ctypes.data, B, out.ctypes.data))
+        self._call(self.lib.qfs_stage_delta, c.ctypes.data, B, out.ctypes.data)
         return out
 
     def stage_matrix(self, delta):
@@ -134,12 +144,12 @@ class Engine:
         B = dl.shape[0]
         n = self.shape.N
         out = np.empty((B, n, n), dtype=np.uint8)
-        self._check(self.lib.qfs_stage_matrix(self._h, dl.ctypes.data, B, out.ctypes.data))
+        self._call(self.lib.qfs_stage_matrix, dl.ctypes.data, B, out.ctypes.data)
         return out
 
     def debug_fill_workspaces(self, byte):
         """Test hook: overwrite every device workspace with `byte` (include/qfs.h)."""
-        self._check(self.lib.qfs_debug_fill_workspaces(self._h, int(byte)))
+        self._call(self.lib.qfs_debug_fill_workspaces, int(byte))
 
     def export_matrix(self, coeffs):
         """Operator matrices [B][N][N] as uint16, the reference's MtsMatrix.entries (mtsmatrix.py:96)."""
@@ -147,7 +157,7 @@ class Engine:
         B = c.shape[0]
         n = self.shape.N
         out = np.empty((B, n, n), dtype="<u2")
-        self._check(self.lib.qfs_export_matrix(self._h, c.ctypes.data, B, out.ctypes.data))
+        self._call(self.lib.qfs_export_matrix, c.ctypes.data, B, out.ctypes.data)
         return out
 
     def stage_matvec_chain(self, M, v0, max_steps, trace=False):
@@ -160,8 +170,8 @@ class Engine:
         hs = np.empty(B, dtype=np.int8)
         its = np.empty(B, dtype=np.int8)
         tr = np.zeros((B, max_steps, n), dtype=np.uint8) if trace else None
-        self._check(self.lib.qfs_stage_matvec_chain(self._h, M.ctypes.data, v0.ctypes.data, B, int(max_steps),
-                                                    tr.ctypes.data if trace else None, hs.ctypes.data, its.ctypes.data))
+        self._call(self.lib.qfs_stage_matvec_chain, M.ctypes.data, v0.ctypes.data, B, int(max_steps),
+                   tr.ctypes.data if trace else None, hs.ctypes.data, its.ctypes.data)
         return (hs, its, tr) if trace else (hs, its)
 
 

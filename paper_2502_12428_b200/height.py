@@ -132,6 +132,10 @@ def _check_batch(p: int, coeffs, bound):
     c = np.asarray(coeffs)
     if c.ndim != 2 or c.shape[1] != NCOEFF:
         raise DomainError(f"coeffs must have shape [B, {NCOEFF}], got {c.shape}")
+    if c.dtype == np.uint8 and c.shape[0] > 4096:
+        # large batches: residues >= p and zero forms are caught by the first kernel of the pipeline (k_fedder raises the input
+        # flag, the library reports QFS_EINVAL, the binding raises DomainError): no host pass over the batch
+        return np.ascontiguousarray(c)
     if c.size and ((c < 0).any() or (c >= p).any()):
         raise DomainError(f"coefficients must lie in [0, {p})")
     c = np.ascontiguousarray(c, dtype=np.uint8)
@@ -153,7 +157,7 @@ def split_blocks(total: int, parts: int):
     return out
 
 
-def height_batch(p: int, coeffs, bound: int = 10, devices=None, method: str = "matrix"):
+def height_batch(p: int, coeffs, bound: int = 10, devices=None, method: str = "matrix", out=None):
     """Heights of B quartics given as rows of `coeffs` (uint8 [B,35], reference basis order).
 
     Returns (heights int8[B], iterations int8[B]) with 0 encoding infinity.  `devices` is a list of
@@ -164,6 +168,7 @@ def height_batch(p: int, coeffs, bound: int = 10, devices=None, method: str = "m
     method: "matrix" (default; builds and streams the operator matrix like the reference's height_matrix) or
     "naive" (the polynomial iteration without the matrix, qfs_heights_free: the on-device counterpart of the
     reference's height_naive cross-check; same heights and iteration counts).
+    out: optional pair of int8[B] numpy arrays to receive the results (e.g. pinned host memory).
     """
     if method not in ("matrix", "naive"):
         raise DomainError(f"unknown method {method!r}, expected 'matrix' or 'naive'")
@@ -171,8 +176,14 @@ def height_batch(p: int, coeffs, bound: int = 10, devices=None, method: str = "m
     from .engine import get_engine
     c = _check_batch(p, coeffs, bound)
     B = c.shape[0]
-    heights = np.empty(B, dtype=np.int8)
-    iters = np.empty(B, dtype=np.int8)
+    if out is not None:
+        heights, iters = out
+        for a in (heights, iters):
+            if not isinstance(a, np.ndarray) or a.dtype != np.int8 or a.shape != (B,) or not a.flags.c_contiguous:
+                raise DomainError(f"out must be a pair of contiguous int8 arrays of length {B}")
+    else:
+        heights = np.empty(B, dtype=np.int8)
+        iters = np.empty(B, dtype=np.int8)
     devs = [0] if devices is None else [int(d) for d in devices]
     if not devs:
         raise DomainError("devices must name at least one GPU")

@@ -73,14 +73,37 @@ class MtsMatrix:
         return f"MtsMatrix({self.rows}x{self.cols} over F_{self.p})"
 
 
-def build_mts(f, p: int, algorithm: str = "wics", device: int = 0) -> MtsMatrix:
-    """Operator matrix of the quartic f over F_p (build_mts(delta1(f^(p-1)), 4(p-1), p), mtsmatrix.py:287-295).
+def build_mts(f, *args, algorithm: str = "wics", device: int = 0) -> MtsMatrix:
+    """Operator matrix over F_p.  Two call forms:
+
+    * `build_mts(delta, d, p, algorithm="wics")` -- the reference's own signature (mtsmatrix.py:287-295): `delta` is the dense
+      Delta_1(g) that `stages.delta1` returned (or any DenseForm of degree p*d: the builder is a generic map Delta -> M);
+    * `build_mts(f, p, algorithm="wics")` -- from the quartic: build_mts(delta1(f^(p-1)), 4(p-1), p) in one call.
 
     `algorithm` is validated like the reference's; TRIV, MERGE and WICS produce the same entries
     (tests/test_mtsmatrix.py in the reference), and the GPU builder is a fourth way to the same matrix.
     """
+    from .stages import DenseForm
+    if isinstance(f, DenseForm) and len(args) >= 2:
+        d, p = int(args[0]), int(args[1])
+        if len(args) >= 3:
+            algorithm = args[2]
+    else:
+        if not args:
+            raise DomainError("build_mts(f, p) needs the prime")
+        d, p = None, int(args[0])
+        if len(args) >= 2:
+            algorithm = args[1]
+        if len(args) >= 3:
+            device = int(args[2])
     if algorithm not in ("triv", "merge", "wics"):
         raise DomainError(f"unknown algorithm {algorithm!r}, expected one of ['merge', 'triv', 'wics']")
+    if d is not None:
+        _check_engine_shape(p)
+        if d != 4 * (p - 1) or f._degree != p * d or f.modulus != p:
+            raise DomainError(f"the GPU engine builds the operator of quartic K3 surfaces: d = 4(p-1), deg delta = p d; got d={d}, deg delta={f._degree}")
+        block = get_engine(p, device).stage_matrix(f.values[None, :])[0]
+        return MtsMatrix(block, NVARS, d, target_degree(d, p * d, NVARS, p), p)
     if hasattr(f, "nvars"):
         SurfaceProblem(p, f.nvars, f)  # the reference's checks (cli.py:110), in its order
         _check_engine_shape(p, f.nvars)

@@ -257,3 +257,99 @@ def test_matrix_free_bounds_fixtures_and_drivers():
     h0, i0 = q.height_batch(11, c)
     h1, i1 = q.height_batch(11, c, method="naive")
     assert np.array_equal(h0, h1) and np.array_equal(i0, i1)
+
+
+def test_reference_named_stage_functions():
+    """power_mod_p / fedder_survives / delta1 / build_mts(delta, d, p) / to_dense / matvec under the reference's names and call
+    forms (qfsplit/__init__.py:11-114; the loop is height_matrix's, height.py:119-144), against the reference's own
+    intermediates (tests/golden/stages_p5.npz)."""
+    import paper_2502_12428_b200 as q
+    p = 5
+    z = np.load(os.path.join(GOLDEN, f"stages_p{p}.npz"))
+    i = [k for k in range(int(z["count"])) if f"s{k}_M" in z.files][0]
+    f = q.Quartic(z[f"s{i}_coeffs"], p)
+    g = q.power_mod_p(f, p - 1)
+    assert np.array_equal(g.values, z[f"s{i}_g"]) and g.degree == 16 and g.modulus == p
+    assert q.fedder_survives(g) == (int(z[f"s{i}_height"]) == 1)
+    delta = q.delta1(g)
+    assert np.array_equal(delta.values, z[f"s{i}_delta"]) and delta.degree == 80
+    m = q.build_mts(delta, 16, p, "wics")
+    assert np.array_equal(m.entries, z[f"s{i}_M"]) and m == q.build_mts(f, p)
+    gv = q.to_dense(g)
+    assert gv.values.dtype == np.uint64
+    cap = 564
+    h, iters = 2, 0
+    while True:       # height.py:135-144
+        gv = q.matvec(m, gv)
+        assert np.array_equal(gv.values, z[f"s{i}_trace"][iters])
+        iters += 1
+        if int(gv.values[cap]) != 0 or h == 10:
+            break
+        h += 1
+    assert iters == int(z[f"s{i}_iters"])
+    with pytest.raises(q.DomainError):
+        q.power_mod_p(f, 3)
+    with pytest.raises(q.DomainError):     # an arbitrary polynomial is not a Witt-carry input here (INTEGRATION.md section 3)
+        q.delta1(q.DenseForm(z[f"s{i}_g"], 16, p))
+    with pytest.raises(q.DomainError):
+        q.build_mts(delta, 16, p, "bogus")
+
+
+@pytest.mark.parametrize("p", [3, 5, 7])
+def test_direct_gather_builder_equals_the_staged_builder_and_the_reference(p, monkeypatch):
+    """Two independent device builders -- k_matrix (QFS_MATRIX_V=4: every thread gathers its entries straight from global Delta)
+    and k_matrix_staged (bulk-copied windows in shared memory) -- produce the reference's matrix (sha256 of the entry block),
+    as the reference pins TRIV = MERGE = WICS on each other (tests/test_acceptance.py:110-125)."""
+    import hashlib
+    from paper_2502_12428_b200.engine import Engine, get_engine
+    z = np.load(os.path.join(GOLDEN, f"stages_p{p}.npz"))
+    idx = [i for i in range(int(z["count"])) if f"s{i}_delta" in z.files]
+    dl = np.stack([z[f"s{i}_delta"] for i in idx])
+    staged = get_engine(p, 0).stage_matrix(dl)
+    monkeypatch.setenv("QFS_MATRIX_V", "4")
+    eng = Engine(p, 0)
+    try:
+        direct = eng.stage_matrix(dl)
+        c = np.stack([z[f"s{i}_coeffs"] for i in range(int(z["count"]))])
+        h4 = eng.heights(c, 10)
+    finally:
+        eng.close()
+    assert np.array_equal(direct, staged)
+    for k, i in enumerate(idx):
+        assert hashlib.sha256(np.ascontiguousarray(direct[k]).tobytes()).digest() == bytes(z[f"s{i}_Msha"])
+    h6 = get_engine(p, 0).heights(c, 10)
+    assert np.array_equal(h4[0], h6[0]) and np.array_equal(h4[1], h6[1])
+    assert [int(h) for h in h6[0]] == [int(z[f"s{i}_height"]) for i in range(int(z["count"]))]
+
+
+def test_stream_order_device_checks_and_shared_engine():
+    """(1) a coefficient tensor written on the default stream right before the call is read after the write (the library orders
+    its stream behind the caller's, the legacy default stream included); (2) large uint8 batches are validated on the device;
+    (3) two threads on one Engine take turns (height_batch(devices=[0, 0])); (4) the caller's current device is left alone."""
+    import torch
+    import paper_2502_12428_b200 as q
+    from paper_2502_12428_b200.engine import get_engine
+    z = np.load(os.path.join(GOLDEN, "heights_p5_seed0_w0_10000.npz"))
+    eng = get_engine(5, 0)
+    src = torch.from_numpy(z["coeffs"]).cuda()
+    for _ in range(5):
+        dev = torch.ones_like(src)                     # stale content: the form x-everything, height known to differ
+        big = torch.empty(64 << 20, device="cuda").normal_()   # keep the default stream busy in front of the copy
+        dev.copy_(src, non_blocking=True)              # queued on the default stream, no synchronisation
+        hs, its = eng.heights(dev, 10)
+        assert np.array_equal(hs.cpu().numpy(), z["heights"]) and np.array_equal(its.cpu().numpy(), z["iters"])
+        del big
+    bad = z["coeffs"].copy()
+    bad[7777, 3] = 9
+    with pytest.raises(q.DomainError):
+        q.height_batch(5, bad)
+    zero = z["coeffs"].copy()
+    zero[4242] = 0
+    with pytest.raises(q.DomainError):
+        q.height_batch(5, zero)
+    hs, its = q.height_batch(5, z["coeffs"], devices=[0, 0])
+    assert np.array_equal(hs, z["heights"]) and np.array_equal(its, z["iters"])
+    out = (np.empty(10000, np.int8), np.empty(10000, np.int8))
+    assert q.height_batch(5, z["coeffs"], out=out)[0] is out[0] and np.array_equal(out[0], z["heights"])
+    assert torch.cuda.current_device() == 0
+    assert eng.stats()["matvec_steps"] == int(z["iters"].astype(np.int64).sum())
