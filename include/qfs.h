@@ -165,6 +165,19 @@ int qfs_cubic_heights(int device, int p, const uint8_t *coeffs, size_t B, int bo
  * device memory. */
 int qfs_export_matrix(qfs_ctx *ctx, const uint8_t *coeffs, size_t B, uint16_t *M16);
 
+/* ---- sampler ----------------------------------------------------------------
+ * The `count` coefficient vectors a worker of the reference's search draws
+ * (search.py:92-98, 103: numpy default_rng([seed, worker]).integers(0, p, 35),
+ * zero draws redrawn), generated on the device: state_inc = {state_hi, state_lo,
+ * inc_hi, inc_lo} of numpy's PCG64 bit generator right after seeding
+ * (np.random.PCG64(np.random.SeedSequence([seed, worker])).state).  coeffs
+ * [count][35] may be host or device memory.  *clean = 1 if the block is the
+ * reference's stream bit for bit; 0 if a draw hit Lemire's rejection branch
+ * (probability p / 2^32 per draw) or a row came out zero: the stream then
+ * shifts from that point on and the caller draws this block on the host. */
+int qfs_sample_quartics(qfs_ctx *ctx, const uint64_t state_inc[4], size_t count, uint8_t *coeffs,
+                        int *clean);
+
 /* ---- test hook -------------------------------------------------------------
  * Overwrites every device workspace the context currently holds with `byte`.
  * No kernel may depend on what a workspace held before the call that uses it

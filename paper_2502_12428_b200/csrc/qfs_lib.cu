@@ -21,6 +21,7 @@
 #include "qfs_matrix.cuh"
 #include "qfs_matrix_staged.cuh"
 #include "qfs_power.cuh"
+#include "qfs_sample.cuh"
 #include "qfs_shape.cuh"
 
 namespace {
@@ -1078,6 +1079,28 @@ int qfs_debug_fill_workspaces(qfs_ctx* ctx, int byte)
     for (DevBuf* b : bufs)
         if (b->ptr) CU(cudaMemsetAsync(b->ptr, byte, b->cap, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
+    return QFS_OK;
+}
+
+int qfs_sample_quartics(qfs_ctx* ctx, const uint64_t state_inc[4], size_t count, uint8_t* coeffs, int* clean)
+{
+    if (!ctx) return QFS_EINVAL;
+    if (!state_inc || !clean || (count && !coeffs)) return fail(ctx, QFS_EINVAL, "NULL buffer");
+    *clean = 1;
+    if (count == 0) return QFS_OK;
+    DeviceGuard guard_(ctx->device);
+    const bool out_dev = is_device_ptr(coeffs);
+    uint8_t* d_out = coeffs;
+    if (!out_dev) { CU(ctx->coeffs.reserve(count * 35)); d_out = ctx->coeffs.as<uint8_t>(); }
+    int* d_flags = ctx->flags.as<int>();
+    CU(cudaMemsetAsync(d_flags, 0, 4 * sizeof(int), ctx->stream));
+    k_sample_quartics<<<(unsigned)((count + 127) / 128), 128, 0, ctx->stream>>>(U128{state_inc[0], state_inc[1]}, U128{state_inc[2], state_inc[3]},
+                                                                               (uint32_t)ctx->p, count, d_out, d_flags);
+    CU(cudaGetLastError());
+    if (!out_dev) CU(cudaMemcpyAsync(coeffs, d_out, count * 35, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(ctx->h_flags, d_flags, 4 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    *clean = ctx->h_flags[0] ? 0 : 1;
     return QFS_OK;
 }
 

@@ -123,6 +123,26 @@ class Engine:
         del keep
         return hs, its
 
+    def sample(self, seed, worker, count, out=None):
+        """The `count` coefficient vectors of worker `worker` of the reference's search (search.py:92-103), drawn on the device.
+
+        Returns (coeffs, clean): coeffs is `out` (a uint8 [count,35] numpy array or torch CUDA tensor) or a new numpy array;
+        clean is False when the block hit one of the stream-shifting events the device only reports (a Lemire rejection, a zero
+        row) -- the caller must then draw the block on the host (search.sample_block)."""
+        bg = np.random.PCG64(np.random.SeedSequence([int(seed), int(worker)]))
+        st = bg.state["state"]
+        mask = (1 << 64) - 1
+        words = (ctypes.c_uint64 * 4)(st["state"] >> 64, st["state"] & mask, st["inc"] >> 64, st["inc"] & mask)
+        if out is None:
+            out = np.empty((int(count), 35), dtype=np.uint8)
+        ptr, keep = _in_ptr(out, (int(count), 35), "out")
+        if _is_torch(out) and out.is_cuda and out.device.index != self.device:
+            raise DomainError(f"tensor on {out.device} handed to the engine of cuda:{self.device}")
+        clean = ctypes.c_int(0)
+        self._call(self.lib.qfs_sample_quartics, words, int(count), ptr, ctypes.byref(clean))
+        del keep
+        return out, bool(clean.value)
+
     # -- stage taps (host numpy in/out) ------------------------------------------------------
     def stage_power(self, coeffs):
         c = np.ascontiguousarray(coeffs, dtype=np.uint8).reshape(-1, 35)

@@ -29,7 +29,7 @@ import numpy as np
 
 from .errors import DomainError, ParseError
 from .height import (INFINITE, HeightResult, SurfaceProblem, decode_height, default_bound, height_batch,
-                     height_matrix, split_blocks)
+                     height_matrix, split_blocks, is_prime)
 from .quartic import NCOEFF, NVARS, Quartic, parse_poly, poly_to_text
 
 
@@ -153,7 +153,8 @@ def sample_block(p: int, count: int, seed: int, worker: int) -> np.ndarray:
 # ---- run_search -------------------------------------------------------------------------------------------
 
 def _finish_block(cfg, start, coeffs, codes):
-    """Histogram / found-log / best of one worker block from its height codes (search.py:104-118)."""
+    """Histogram / found-log / best of one worker block from its height codes (search.py:104-118).  `coeffs` is anything
+    indexable by row that yields the 35 coefficients (a numpy array, a torch tensor on the device)."""
     bound = cfg.bound if cfg.bound is not None else default_bound(cfg.n)
     used = len(codes)
     if cfg.target_height is not None:
@@ -170,23 +171,53 @@ def _finish_block(cfg, start, coeffs, codes):
     prev = np.concatenate(([0], run[:-1])) if used else run
     for i in np.nonzero((finite > prev) & (finite > 0))[0]:
         best = int(finite[i])
-        found.append(FoundSurface(start + int(i), best, Quartic(coeffs[i], cfg.p)))
+        found.append(FoundSurface(start + int(i), best, Quartic(_row(coeffs, int(i)), cfg.p)))
     return hist, found, best
+
+
+def _row(coeffs, i):
+    r = coeffs[i]
+    return r.cpu().numpy() if hasattr(r, "cpu") else np.asarray(r)
+
+
+def device_block(p: int, count: int, seed: int, worker: int, device: int = 0, bound: int = 10, method: str = "matrix"):
+    """One worker block entirely on the GPU: the coefficient vectors are drawn on the device (csrc/qfs_sample.cuh: numpy's PCG64
+    stream of default_rng([seed, worker]) jumped ahead per row), the heights are computed there, and only the height codes come
+    back.  Returns (coeffs, codes, iters): coeffs is a torch CUDA tensor [count,35] (rows are fetched on demand), or a numpy array
+    when the device reported a stream-shifting event (a Lemire rejection or a zero draw: about one block in 200 at 100 000
+    rows) and the block was redrawn on the host -- either way the reference's samples, bit for bit."""
+    import torch
+    from .engine import get_engine
+    from .height import _check_engine_shape
+    if not is_prime(p):
+        raise DomainError(f"p={p} is not prime")
+    _check_engine_shape(p)
+    if method not in ("matrix", "naive"):
+        raise DomainError(f"unknown method {method!r}, expected 'matrix' or 'naive'")
+    eng = get_engine(p, device)
+    dev = torch.empty((count, NCOEFF), dtype=torch.uint8, device=f"cuda:{device}")
+    _, clean = eng.sample(seed, worker, count, out=dev)
+    if not clean:
+        host = sample_block(p, count, seed, worker)
+        codes, iters = eng.heights(host, int(bound), matrix_free=(method == "naive"))
+        return host, codes, iters
+    hs, its = eng.heights(dev, int(bound), matrix_free=(method == "naive"))
+    return dev, hs.cpu().numpy(), its.cpu().numpy()
 
 
 def worker_block(cfg: SearchConfig, worker: int, start: int, count: int, device: int = 0, compute=None):
     """GPU counterpart of search._worker_block: sample the block, one batched height call, summarise.
 
-    `compute(p, coeffs, bound, device) -> (codes, iters)` defaults to the CUDA engine; tests inject the CPU
-    oracle here to exercise the host logic without a GPU.
+    On the engine the block never leaves the device (device_block).  `compute(p, coeffs, bound, device) -> (codes, iters)`
+    replaces the engine in the CPU tests (the C oracle), with the block sampled on the host.
     """
     bound = cfg.bound if cfg.bound is not None else default_bound(cfg.n)
     if cfg.n != NVARS:
         raise DomainError(f"the GPU engine handles quartics in 4 variables; got n={cfg.n}")
-    coeffs = sample_block(cfg.p, count, cfg.rng_seed, worker)
     if compute is None:
-        codes, _ = height_batch(cfg.p, coeffs, bound, devices=[device])
+        coeffs, codes, _ = device_block(cfg.p, count, cfg.rng_seed, worker, device, bound)
     else:
+        coeffs = sample_block(cfg.p, count, cfg.rng_seed, worker)
         codes, _ = compute(cfg.p, coeffs, bound, device)
     return _finish_block(cfg, start, coeffs, np.asarray(codes))
 
@@ -244,62 +275,38 @@ def spectrum_search(p: int, block: int = 100000, rng_seed: int = 0, bound: int =
     """Sample seeded blocks until every height in `want` (default 1..bound and infinity) has a witness.
 
     Block b uses the reference stream `default_rng([rng_seed, b])`, so any witness can be regenerated from
-    (rng_seed, b, index).  Blocks are sampled on a host thread ahead of the GPUs (one consumer thread per
-    device) and retired in block order, so the result does not depend on the number of devices.
+    (rng_seed, b, index).  One host thread per device takes the next block number, has the block sampled AND solved on its
+    GPU (device_block: nothing but the height codes crosses the bus) and the blocks are retired in block order, so the result
+    does not depend on the number of devices and the host does no per-sample work.
     Returns (witnesses {height code: (block, index, Quartic)}, HeightHistogram, blocks_done); height code
     0 = infinity.  `progress(blocks_done, hist, witnesses)` is called after every retired block.
     `method` = "matrix" (operator matrix built and streamed) or "naive" (matrix-free iteration); same heights.
     """
-    import queue
     devs = [0] if devices is None else [int(d) for d in devices]
     want = set(range(0, bound + 1)) if want is None else {0 if (isinstance(h, float) and math.isinf(h)) else int(h) for h in want}
     hist = HeightHistogram(bound)
     witnesses = {}
-    todo = queue.Queue(maxsize=2 * len(devs))
     done = {}
     cond = threading.Condition()
     stop = threading.Event()
     errors = []
-
-    def produce():
-        try:
-            for blk in range(max_blocks):
-                if stop.is_set():
-                    break
-                item = (blk, sample_block(p, block, rng_seed, blk))
-                while not stop.is_set():
-                    try:
-                        todo.put(item, timeout=0.05)
-                        break
-                    except queue.Full:
-                        pass
-        except Exception as exc:
-            errors.append(exc)
-        finally:
-            for _ in devs:
-                while True:
-                    try:
-                        todo.put(None, timeout=0.05)
-                        break
-                    except queue.Full:
-                        if stop.is_set():
-                            try:
-                                todo.get_nowait()
-                            except queue.Empty:
-                                pass
+    ticket = [0]            # next block number; a consumer takes one at a time, at most 2 per device ahead of the retired front
+    front = [0]
 
     def consume(dev):
         try:
-            while True:
-                item = todo.get()
-                if item is None:
-                    break
-                blk, coeffs = item
-                if stop.is_set():
-                    continue
+            while not stop.is_set():
+                with cond:
+                    while ticket[0] - front[0] >= 2 * len(devs) and not stop.is_set():
+                        cond.wait(timeout=0.1)
+                    if stop.is_set() or ticket[0] >= max_blocks:
+                        break
+                    blk = ticket[0]
+                    ticket[0] += 1
                 if compute is None:
-                    codes, _ = height_batch(p, coeffs, bound, devices=[dev], method=method)
+                    coeffs, codes, _ = device_block(p, block, rng_seed, blk, dev, bound, method)   # sampled and solved on the GPU
                 else:
+                    coeffs = sample_block(p, block, rng_seed, blk)
                     codes, _ = compute(p, coeffs, bound, dev)
                 with cond:
                     done[blk] = (coeffs, np.asarray(codes))
@@ -309,7 +316,7 @@ def spectrum_search(p: int, block: int = 100000, rng_seed: int = 0, bound: int =
             with cond:
                 cond.notify_all()
 
-    threads = [threading.Thread(target=produce, daemon=True)] + [threading.Thread(target=consume, args=(d,), daemon=True) for d in devs]
+    threads = [threading.Thread(target=consume, args=(d,), daemon=True) for d in devs]
     for t in threads:
         t.start()
     nxt = 0
@@ -325,8 +332,11 @@ def spectrum_search(p: int, block: int = 100000, rng_seed: int = 0, bound: int =
             h = int(h)
             if h not in witnesses:
                 i = int(np.nonzero(codes == h)[0][0])
-                witnesses[h] = (nxt, i, Quartic(coeffs[i], p))
+                witnesses[h] = (nxt, i, Quartic(_row(coeffs, i), p))
         nxt += 1
+        with cond:
+            front[0] = nxt
+            cond.notify_all()
         if progress is not None:
             progress(nxt, hist, witnesses)
     stop.set()

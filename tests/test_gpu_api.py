@@ -353,3 +353,48 @@ def test_stream_order_device_checks_and_shared_engine():
     assert q.height_batch(5, z["coeffs"], out=out)[0] is out[0] and np.array_equal(out[0], z["heights"])
     assert torch.cuda.current_device() == 0
     assert eng.stats()["matvec_steps"] == int(z["iters"].astype(np.int64).sum())
+
+
+def test_device_sampler_reproduces_the_reference_stream():
+    """qfs_sample_quartics against the host sampler (which is pinned on the reference's own seeded dumps, tests/test_host_api.py):
+    identical blocks for several primes / seeds / workers / sizes, into host and device memory; and the one thing the device
+    only reports -- block (seed 0, worker 65) over F_13 holds a Lemire rejection at draw 541 684 -- is reported, and
+    device_block falls back to the host stream for it."""
+    import torch
+    import paper_2502_12428_b200 as q
+    from paper_2502_12428_b200.engine import get_engine
+    from paper_2502_12428_b200.search import device_block
+    for p, seed, w, n in ((5, 0, 0, 100000), (5, 0, 3, 777), (7, 12, 5, 50001), (11, 1, 0, 4000), (13, 0, 64, 20000), (3, 5, 1, 1)):
+        got, clean = get_engine(p, 0).sample(seed, w, n)
+        assert clean and np.array_equal(got, q.sample_block(p, n, seed, w)), (p, seed, w, n)
+    dev = torch.empty((30000, 35), dtype=torch.uint8, device="cuda:0")
+    _, clean = get_engine(7, 0).sample(2, 9, 30000, out=dev)
+    assert clean and np.array_equal(dev.cpu().numpy(), q.sample_block(7, 30000, 2, 9))
+    _, clean = get_engine(13, 0).sample(0, 65, 100000)
+    assert not clean
+    _, clean = get_engine(13, 0).sample(0, 65, 15000)      # the rejection sits behind row 15 000: this prefix is clean
+    assert clean
+    coeffs, codes, its = device_block(13, 100000, 0, 65)
+    assert isinstance(coeffs, np.ndarray) and np.array_equal(coeffs, q.sample_block(13, 100000, 0, 65))
+    hs, _ = q.height_batch(13, coeffs[:3000], method="naive")
+    assert np.array_equal(codes[:3000], hs)
+
+
+def test_spectrum_search_on_the_gpu_and_its_witnesses():
+    """SURVEY 8(f)1 / BASELINE configs[3] at F_5: sample seeded blocks until every height 1..10 and infinity has a witness (blocks
+    drawn and solved on the device), then re-verify every witness with the CPU oracle and regenerate it from (seed, block, index)."""
+    import oracle
+    import paper_2502_12428_b200 as q
+    wit, hist, blocks = q.spectrum_search(5, block=100000, rng_seed=0, max_blocks=400)
+    assert set(wit) == set(range(0, 11)) and hist.total == 100000 * blocks
+    for code, (blk, i, f) in wit.items():
+        oh, _ = oracle.heights_batch(f.coeffs[None, :], 5, 10)
+        assert int(oh[0]) == code
+        assert np.array_equal(q.sample_block(5, i + 1, 0, blk)[i], f.coeffs)
+    rows = q.spectrum_rows(wit).splitlines()
+    assert len(rows) == 11 and rows[-1].startswith("5 ; inf ;")
+    verdicts = q.verify_fixtures(q.spectrum_rows(wit))
+    assert all(v.ok for v in verdicts)
+    # the matrix-free mode finds the same witnesses (same blocks, same heights)
+    wit2, hist2, blocks2 = q.spectrum_search(5, block=100000, rng_seed=0, max_blocks=400, method="naive")
+    assert blocks2 == blocks and {h: w[:2] for h, w in wit2.items()} == {h: w[:2] for h, w in wit.items()}

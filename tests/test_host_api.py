@@ -182,3 +182,35 @@ def test_verify_fixtures_and_spectrum():
         assert int(p_s) == 3 and h_s == ("inf" if h == 0 else str(h))
         f = q.parse_poly(poly, 4, 3)
         assert oracle.height_matrix(f.coeffs, 3, 10)[0] == h
+
+
+def test_sampler_stream_arithmetic_in_python_integers():
+    """The arithmetic of csrc/qfs_sample.cuh, written in Python integers, against numpy's generator: PCG64 = 128-bit LCG stepped
+    BEFORE the XSL-RR output, jump-ahead by the (multiplier, increment) doubling recurrence, two 32-bit draws per output (low half
+    first), Lemire multiply-shift to [0, p).  (search.py:92-103 draws rng.integers(0, p, size=35) from default_rng([seed, w]).)"""
+    A, M = 0x2360ED051FC65DA44385DF649FCCF645, (1 << 128) - 1
+
+    def out(s):
+        x, r = ((s >> 64) ^ s) & 0xFFFFFFFFFFFFFFFF, s >> 122
+        return ((x >> r) | (x << (64 - r))) & 0xFFFFFFFFFFFFFFFF if r else x
+
+    def advance(s, inc, delta):
+        am, ap, cm, cp = 1, 0, A, inc
+        while delta:
+            if delta & 1:
+                am, ap = (am * cm) & M, (ap * cm + cp) & M
+            cp, cm, delta = ((cm + 1) * cp) & M, (cm * cm) & M, delta >> 1
+        return (am * s + ap) & M
+
+    for p, seed, w in ((5, 0, 0), (7, 3, 2), (11, 9, 1), (13, 0, 65)):
+        st = np.random.PCG64(np.random.SeedSequence([seed, w])).state["state"]
+        want = np.random.default_rng([seed, w]).integers(0, p, size=(40, 35))
+        for r in (0, 1, 17, 39):
+            s = advance(st["state"], st["inc"], (35 * r) >> 1)
+            vals = []
+            for _ in range(19):
+                s = (s * A + st["inc"]) & M
+                o = out(s)
+                vals += [o & 0xFFFFFFFF, o >> 32]
+            row = [(v * p) >> 32 for v in vals[(35 * r) & 1:][:35]]
+            assert row == want[r].tolist()
