@@ -30,7 +30,27 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-PAPER_RATE = {5: 1400.0, 7: 180.0}  # BASELINE.md section 1 (2080 Ti), surfaces that take the full operator path
+# surfaces/s that take the full operator path: F_5, F_7 on a 2080 Ti; F_11: one surface per 39-40 s on an RTX 3090
+PAPER_RATE = {5: 1400.0, 7: 180.0, 11: 1.0 / 39.5}
+PAPER_NOTE = {5: "~1400/s on a 2080 Ti", 7: "~180/s on a 2080 Ti", 11: "one surface per 39-40 s (0.025/s) on an RTX 3090"}
+
+
+def reference_python_rate(p):
+    """Rate of the UNMODIFIED reference (qfsplit, numpy + numba) measured in the authoring container (tools/measure_reference.py):
+    it does not travel to the GPU box, so the box-side CPU arm is its C port and this is quoted beside it."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "reference_python_rate.json")) as fh:
+            j = json.load(fh)
+        e = j[f"F_{p}"]
+        return {"surfaces_per_s": e["surfaces_per_s"], "surfaces_per_s_per_core": e["surfaces_per_s_per_core"], "cores": j["cores"],
+                "samples": e["samples"], "where": "authoring container, profiles/reference_python_rate.json"}
+    except Exception:
+        return None
+
+
+def workload_name(p, batch):
+    N, _ = SHAPES[p]
+    return f"{batch} seeded random quartics over F_{p} per GPU ({N}x{N} operator), bound 10"
 SHAPES = {3: (165, 2925), 5: (969, 91881), 7: (2925, 818805), 11: (12341, 14391741)}  # N, L
 
 
@@ -67,14 +87,18 @@ def measured_peaks():
 
 
 def measured_traffic(p, kernel, hard, launches):
-    """dram__bytes_read.sum + dram__bytes_write.sum of `kernel` per launch, scaled from the committed
-    `ncu --set full` capture (profiles/traffic.json: bytes per hard surface measured on a 4000-hard-surface
-    launch) to this run's surfaces per launch; None if no capture is on file."""
+    """dram__bytes_read.sum + dram__bytes_write.sum of `kernel` per launch from the committed `ncu --set full` capture
+    (profiles/traffic.json).  The capture of the headline configuration is taken AT the benchmark's launch size (its `hard`
+    equals this run's surfaces per launch: the number is the measured one); otherwise it is the capture's bytes per hard surface
+    times this run's surfaces per launch.  None if no capture is on file."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
             t = json.load(fh)
-        per = t[f"p{p}"][kernel]["dram_bytes_per_hard_surface"]
-        return per * hard / launches
+        e = t[f"p{p}"][kernel]
+        per_launch = hard / launches
+        if abs(e.get("hard_surfaces_in_capture", 0) - per_launch) <= 0.001 * per_launch:
+            return e["dram_bytes_per_launch"]
+        return e["dram_bytes_per_hard_surface"] * per_launch
     except Exception:
         return None
 
@@ -239,8 +263,9 @@ def run_reference_arm(args):
         "impl": "reference", "metric": "quartic K3 heights/sec", "value": val, "unit": "surfaces/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": f"{args.batch} seeded random quartics over F_{p} (sampled: {n}/step)", "p": p, "bound": 10},
-        "cpu_baseline": {"value": val, "unit": "surfaces/s", "cores": threads, "kind": "port", "sample": sample},
+        "config": {"workload": workload_name(p, args.batch), "p": p, "bound": 10},
+        "cpu_baseline": {"value": val, "unit": "surfaces/s", "cores": threads, "kind": "port", "sample": sample,
+                         "reference_python": reference_python_rate(p)},
         "e2e": {"value": val, "unit": "surfaces/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -279,28 +304,30 @@ def measure_gpu(p, batch, steps, warmup, seed, rank, world, device, dist):
         launches += st["kernel_launches"]
     e1.record()
     barrier()
-    clocks = sampler.stop()
     ms = e0.elapsed_time(e1)
     st = eng.stats()
 
-    # end to end through the public API with pinned host buffers
+    # end to end through the PUBLIC entry (height_batch: argument checks, host -> device copy of the batch, the pipeline, device ->
+    # host copy of the results) with pinned host buffers; the clock sampler keeps running: same kernels, same load
+    from paper_2502_12428_b200 import height_batch
     h_hs = torch.empty(batch, dtype=torch.int8).pin_memory().numpy()
     h_its = torch.empty(batch, dtype=torch.int8).pin_memory().numpy()
     h_in = pinned.numpy()
     e2e_steps = max(1, min(steps, 10))
-    eng.heights(h_in, 10, out=(h_hs, h_its))
+    height_batch(p, h_in, 10, devices=[device], out=(h_hs, h_its))
     barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        eng.heights(h_in, 10, out=(h_hs, h_its))
+        height_batch(p, h_in, 10, devices=[device], out=(h_hs, h_its))
     torch.cuda.synchronize(device)
     e2e_s = time.perf_counter() - t0
+    clocks = sampler.stop()
 
     heights = hs.cpu().numpy()
     iters = its.cpu().numpy()
     assert np.array_equal(heights, h_hs) and np.array_equal(iters, h_its)
     if dist is not None:
-        t = torch.tensor([ms, e2e_s], dtype=torch.float64, device=dev.device)
+        t = torch.tensor([ms, e2e_s], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, e2e_s = float(t[0]), float(t[1])
     return {"ms": ms, "e2e_s": e2e_s, "e2e_steps": e2e_steps, "stage": stage, "launches": launches, "stats": st,
@@ -378,7 +405,7 @@ def gpu_line(args, p, res, world, with_cpu):
     ms_step = res["ms"] / steps
     value = world * batch * steps / (res["ms"] * 1e-3)
     stage = {k: v / steps for k, v in res["stage"].items()}
-    kernels = {"delta": ("k_delta", stage["ms_delta"], ab["delta"]),
+    kernels = {"delta": ("k_delta_mma", stage["ms_delta"], ab["delta"]),
                "matrix": ("k_matrix_staged", stage["ms_matrix"], ab["matrix"]),
                "matvec": ("k_chain" if p <= 7 else "k_chain_grid", stage["ms_matvec"], ab["matvec"])}
     top = max(kernels, key=lambda k: kernels[k][1])
@@ -392,10 +419,10 @@ def gpu_line(args, p, res, world, with_cpu):
         "vs_baseline": (value * hard / batch) / PAPER_RATE[p] if p in PAPER_RATE else None,
         "dtype": "u8", "data": "synthetic",
         "config": {
-            "workload": f"{batch} seeded random quartics over F_{p} per GPU ({N}x{N} operator), bound 10",
+            "workload": workload_name(p, batch),
             "p": p, "batch_per_gpu": batch, "seed": args.seed, "parallelism": f"{world} independent shards, no collective",
             "l2": f"working set per step {ab['total'] / 1e9:.1f} GB >> 126 MB L2 (no flush needed)",
-            "vs_baseline_note": "hard (height>=2) surfaces/s over the paper's ~%d/s on a 2080 Ti (BASELINE.md s1)" % PAPER_RATE.get(p, 0),
+            "vs_baseline_note": "hard (height>=2) surfaces/s over the paper's " + PAPER_NOTE.get(p, "(no published figure)") + " (BASELINE.md s1)",
         },
         "hard_fraction": hard / batch,
         "hard_per_s": value * hard / batch,
@@ -409,7 +436,8 @@ def gpu_line(args, p, res, world, with_cpu):
         "roofline_pipeline": {"algorithmic_bytes_per_step": ab["total"], "achieved": ab["total"] / (ms_step * 1e-3) / 1e9,
                               "peak": peak, "unit": "GB/s", "frac": ab["total"] / (ms_step * 1e-3) / 1e9 / peak},
         "e2e": {"value": world * batch * res["e2e_steps"] / res["e2e_s"], "unit": "surfaces/s",
-                "h2d_bytes_per_step": batch * 35, "d2h_bytes_per_step": 2 * batch},
+                "h2d_bytes_per_step": batch * 35, "d2h_bytes_per_step": 2 * batch,
+                "through": "paper_2502_12428_b200.height_batch (the public entry), pinned host buffers"},
         "gpu_launches": int(res["launches"]),
         "clocks": res["clocks"],
     }
@@ -417,6 +445,7 @@ def gpu_line(args, p, res, world, with_cpu):
         cb, ohs = cpu_baseline(p, res["coeffs"], args.cpu_seconds)
         n = len(ohs)
         cb["parity_on_sample"] = bool(np.array_equal(ohs, heights[:n]))
+        cb["reference_python"] = reference_python_rate(p)
         line["cpu_baseline"] = cb
     return line
 
@@ -448,7 +477,7 @@ def main():
         import torch.distributed as dist_mod
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         torch.cuda.set_device(local)
-        dist_mod.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        dist_mod.init_process_group("gloo")   # a barrier and one 2-double max: the path itself has no collective (no NCCL)
         dist = dist_mod
     elif args.gpus > 1 and "RANK" not in os.environ:
         # convenience: relaunch under torchrun
@@ -483,8 +512,8 @@ def main():
         saved = args.batch
         args.batch = b11
         close_all()
-        res11 = measure_gpu(11, b11, 2, 3, args.seed, rank, world, local, dist)
-        res11["steps"] = 2
+        res11 = measure_gpu(11, b11, 5, 3, args.seed, rank, world, local, dist)
+        res11["steps"] = 5
         if rank == 0:
             l11 = gpu_line(args, 11, res11, world, with_cpu=False)
             line["also"]["F_11"] = {k: l11[k] for k in keep if k in l11}

@@ -24,10 +24,11 @@ tag = sys.argv[1]
 shutil.copy(os.path.join(OUT, f"bench_{tag}.json"), os.path.join(HERE, f"{tag}_bench_line.json"))
 shutil.copy(os.path.join(OUT, f"bench_{tag}_ref.json"), os.path.join(HERE, f"{tag}_bench_reference_arm.json"))
 shutil.copy(os.path.join(OUT, f"launches_{tag}.csv"), os.path.join(HERE, f"{tag}_launches_p5_p7_p11.csv"))
-for p in (5, 7):
-    txt = subprocess.run([sys.executable, os.path.join(HERE, "ncu_summary.py"), os.path.join(OUT, f"{tag}_full_p{p}.ncu-rep")],
-                         capture_output=True, text=True).stdout
-    open(os.path.join(HERE, f"{tag}_ncu_full_p{p}.txt"), "w").write(txt)
+# The reports are reduced on the GPU box (they exceed what gpurun copies back): {tag}_full_pP.{summary.txt, lines.txt, raw.csv}
+PRIMES = [p for p in (5, 7, 11) if os.path.exists(os.path.join(OUT, f"{tag}_full_p{p}.raw.csv"))]
+for p in PRIMES:
+    shutil.copy(os.path.join(OUT, f"{tag}_full_p{p}.summary.txt"), os.path.join(HERE, f"{tag}_ncu_full_p{p}.txt"))
+    shutil.copy(os.path.join(OUT, f"{tag}_full_p{p}.lines.txt"), os.path.join(HERE, f"{tag}_ncu_lines_p{p}.txt"))
 
 rows = [r for r in csv.reader(open(os.path.join(OUT, f"launches_{tag}.csv"))) if len(r) > 5]
 hdr, agg = None, collections.OrderedDict()
@@ -59,18 +60,26 @@ tot = collections.Counter()
 for k in contract:
     tot[prime(k)] += agg[k][1]
 with open(os.path.join(HERE, f"{tag}_launches_summary.csv"), "w") as fh:
-    fh.write("# ncu --metrics gpu__time_duration.sum --clock-control none -c 700, command: python bench.py --steps 2 --warmup 1 --cpu-seconds 1\n")
-    fh.write("# (bench.py clamps warm-up to 3: F_5 3 warm-up + 2 timed + e2e calls, then F_7, F_11, then the matrix-free calls; the capture stops at 700 launches).\n")
+    fh.write("# ncu --metrics gpu__time_duration.sum --clock-control none -c 900, command: python bench.py --steps 2 --warmup 1 --cpu-seconds 1\n")
+    fh.write("# (bench.py clamps warm-up to 3: F_5 3 warm-up + 2 timed + e2e calls, then F_7, F_11, then the matrix-free calls; the capture stops at 900 launches).\n")
     fh.write("# Times are cold-cache and serialised by the profiler: compare SHARES per prime with bench.py stage_ms_per_step, not absolutes.\n")
     fh.write("# k_fedder / k_power_full also run in the matrix-free calls, so their share is overstated where k_free appears.\n")
     fh.write("kernel,launches,total_ms,share_of_same_prime\n")
     for k, (n, ms) in agg.items():
         fh.write(f"{k},{n},{ms:.3f},{(ms / tot[prime(k)] if k in contract and tot[prime(k)] else 0):.3f}\n")
 
-traffic = {}
-for p, hard in ((5, 4000), (7, 2792)):
-    txt = subprocess.run(["ncu", "-i", os.path.join(OUT, f"{tag}_full_p{p}.ncu-rep"), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-    rows = list(csv.reader(txt.splitlines()))
+def hard_and_batch(p):   # the capture's launch size, from the stats line profiles/run_profile.py prints
+    log = open(os.path.join(OUT, f"{tag}_full_p{p}.log")).read()
+    return int(re.findall(r"'hard': (\d+)", log)[-1]), int(re.findall(r"'surfaces': (\d+)", log)[-1])
+
+
+try:
+    traffic = json.load(open(os.path.join(HERE, "traffic.json")))
+except Exception:
+    traffic = {}
+for p in PRIMES:
+    hard, batch = hard_and_batch(p)
+    rows = list(csv.reader(open(os.path.join(OUT, f"{tag}_full_p{p}.raw.csv")).read().splitlines()))
     h, units = rows[0], rows[1]
     traffic[f"p{p}"] = {}
     for r in rows[2:]:
@@ -81,9 +90,9 @@ for p, hard in ((5, 4000), (7, 2792)):
                     "usecond": 1e-3, "msecond": 1}.get(units[h.index(k)], 1)
             return float(r[h.index(k)].replace(",", "")) * mult
         rd, wr, t = val("dram__bytes_read.sum"), val("dram__bytes_write.sum"), val("gpu__time_duration.sum")
-        traffic[f"p{p}"][key] = {"dram_bytes_per_hard_surface": (rd + wr) / hard, "dram_read": rd, "dram_write": wr,
-                                 "hard_surfaces_in_launch": hard, "gpu_time_ms": t,
-                                 "source": f"profiles/{tag}_ncu_full_p{p}.txt (ncu --set full, clock-control none, profiles/run_profile.py --p {p} --batch 20000 --calls 1)"}
+        traffic[f"p{p}"][key] = {"dram_bytes_per_hard_surface": (rd + wr) / hard, "dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
+                                 "hard_surfaces_in_capture": hard, "gpu_time_ms": t,
+                                 "source": f"profiles/{tag}_ncu_full_p{p}.txt (ncu --set full, clock-control none, profiles/run_profile.py --p {p} --batch {batch} --calls 2, second call)"}
 json.dump(traffic, open(os.path.join(HERE, "traffic.json"), "w"), indent=1)
 d = json.loads(open(os.path.join(HERE, f"{tag}_bench_line.json")).read().strip().splitlines()[-1])
 print("F_5", round(d["value"]), {k: round(v, 3) for k, v in d["stage_ms_per_step"].items()}, "frac", round(d["roofline"]["frac"], 3), "e2e", round(d["e2e"]["value"]))

@@ -27,7 +27,7 @@ for r in rows:
         lines.append((cur_file, int(r[0]), r[1].strip(), col('Instructions Executed'), col('# Samples'), col('L1 Wavefronts Shared')))
 ti = sum(l[3] for l in lines) or 1
 ts = sum(l[4] for l in lines) or 1
-print(f'total warp instructions {ti}, samples {ts}')
+print(f'total warp instructions {ti}, samples {ts} (all kernels of the report; lines of a file shared by several kernels are summed)')
 print('--- by instructions executed')
 for l in sorted(lines, key=lambda x: -x[3])[:top]:
     print(f'{100*l[3]/ti:5.1f}% inst {100*l[4]/ts:5.1f}% smp  smem_wf {l[5]:>10d}  {l[0]}:{l[1]:<4d} {l[2][:110]}')
