@@ -155,6 +155,14 @@ int qfs_stage_matvec_chain(qfs_ctx *ctx, const uint8_t *M, const uint8_t *v0, si
 int qfs_cubic_heights(int device, int p, const uint8_t *coeffs, size_t B, int bound,
                       int8_t *heights, int8_t *iters);
 
+/* Heights of B forms of degree n in n variables, n = 2..6 (height.py:63-144 accept any n >= 2; the quartic context
+ * and qfs_cubic_heights cover n = 4 and n = 3 at full speed, this is the general entry at toy sizes:
+ * (n p + 1)^(n-1) <= 2^24).  coeffs[B][C(2n-1, n-1)]: the coefficients over MonomialBasis(n, n) of the reference,
+ * lex-ascending with x1 most significant (monomials.py:182-196).  Matrix-free iteration; heights and iteration
+ * counts are those of height_matrix and height_naive.  Context-free like qfs_cubic_heights. */
+int qfs_form_heights(int device, int p, int n, const uint8_t *coeffs, size_t B, int bound,
+                     int8_t *heights, int8_t *iters);
+
 /* ---- export ---------------------------------------------------------------
  * Operator matrices of B quartics (given by their coefficient vectors) in the
  * reference's export layout: M16[B][N][N] row-major uint16 little-endian --

@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -17,6 +18,7 @@
 #include "qfs_delta.cuh"
 #include "qfs_delta_direct.cuh"
 #include "qfs_delta_mma.cuh"
+#include "qfs_form.cuh"
 #include "qfs_free.cuh"
 #include "qfs_matrix.cuh"
 #include "qfs_matrix_staged.cuh"
@@ -1059,6 +1061,84 @@ int qfs_cubic_heights(int device, int p, const uint8_t* coeffs, size_t B, int bo
     CUC(cudaFuncSetAttribute(k_cubic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_cubic<<<(unsigned)B, QFS_CUBIC_NT, smem>>>(d_c, (int)B, p, bound - 1, d_h, d_i, d_err);
     CUC(cudaGetLastError());
+    CUC(cudaMemcpy(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost));
+    if (!h_dev) CUC(cudaMemcpy(heights, d_h, B, cudaMemcpyDeviceToHost));
+    if (!i_dev) CUC(cudaMemcpy(iters, d_i, B, cudaMemcpyDeviceToHost));
+    CUC(cudaDeviceSynchronize());
+#undef CUC
+    cleanup();
+    if (h_err & QFS_ERRBIT_INPUT) return fail(ctx, QFS_EINVAL, "input violates a precondition: a coefficient >= p or the zero form");
+    if (h_err & QFS_ERRBIT_INVARIANT) return fail(ctx, QFS_EINVARIANT, "Witt-carry numerator not divisible by p");
+    return QFS_OK;
+}
+
+int qfs_form_heights(int device, int p, int n, const uint8_t* coeffs, size_t B, int bound, int8_t* heights, int8_t* iters)
+{
+    qfs_ctx* ctx = nullptr;  // errors of this context-free entry go where qfs_create's go: qfs_last_error(NULL)
+    if (n < 2 || n > QFS_FORM_MAXN) return fail(ctx, QFS_EINVAL, "forms in n = 2..%d variables, got n=%d", QFS_FORM_MAXN, n);
+    if (p < 3 || p > QFS_FORM_MAXP || p % 2 == 0) return fail(ctx, QFS_EINVAL, "p=%d is not an odd prime <= %d", p, QFS_FORM_MAXP);
+    for (int q = 3; q * q <= p; q += 2)
+        if (p % q == 0) return fail(ctx, QFS_EINVAL, "p=%d is not prime", p);
+    {
+        double box = 1;
+        for (int i = 0; i < n - 1; ++i) box *= (double)(n * p + 1);
+        if (box > (double)QFS_FORM_MAXBOX) return fail(ctx, QFS_EINVAL, "n=%d, p=%d: (n p + 1)^(n-1) exceeds 2^24 entries", n, p);
+    }
+    if (bound < 1 || bound > 127) return fail(ctx, QFS_EINVAL, "bound must be in 1..127, got %d", bound);
+    if (B == 0) return QFS_OK;
+    if (!coeffs || !heights || !iters) return fail(ctx, QFS_EINVAL, "NULL buffer");
+    if (B > 0x7fffffffULL) return fail(ctx, QFS_EINVAL, "batch too large");
+    // basis(n, n) in lex-ascending order, x1 most significant (monomials.py:182-196)
+    std::vector<uint8_t> ex;
+    {
+        std::vector<int> e(n, 0);
+        std::function<void(int, int)> rec = [&](int i, int left) {
+            if (i == n - 1) { e[i] = left; for (int v : e) ex.push_back((uint8_t)v); return; }
+            for (int a = 0; a <= left; ++a) { e[i] = a; rec(i + 1, left - a); }
+        };
+        rec(0, n);
+    }
+    const int nterms = (int)(ex.size() / n);
+    DeviceGuard guard_(device);
+    const bool in_dev = is_device_ptr(coeffs), h_dev = is_device_ptr(heights), i_dev = is_device_ptr(iters);
+    uint8_t *d_c = nullptr, *d_ex = nullptr, *d_scratch = nullptr;
+    int8_t *d_h = nullptr, *d_i = nullptr;
+    int* d_err = nullptr;
+    int rc = QFS_OK, h_err = 0;
+    auto cleanup = [&]() {
+        if (!in_dev && d_c) cudaFree(d_c);
+        if (!h_dev && d_h) cudaFree(d_h);
+        if (!i_dev && d_i) cudaFree(d_i);
+        if (d_ex) cudaFree(d_ex);
+        if (d_scratch) cudaFree(d_scratch);
+        if (d_err) cudaFree(d_err);
+    };
+#define CUC(call)                                                                                          \
+    do {                                                                                                   \
+        cudaError_t e_ = (call);                                                                           \
+        if (e_ != cudaSuccess) {                                                                           \
+            rc = fail(ctx, e_ == cudaErrorMemoryAllocation ? QFS_ENOMEM : QFS_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+            cleanup();                                                                                     \
+            return rc;                                                                                     \
+        }                                                                                                  \
+    } while (0)
+    const size_t row = (size_t)nterms;
+    if (in_dev) d_c = const_cast<uint8_t*>(coeffs);
+    else { CUC(cudaMalloc(&d_c, B * row)); CUC(cudaMemcpy(d_c, coeffs, B * row, cudaMemcpyHostToDevice)); }
+    if (h_dev) d_h = heights; else CUC(cudaMalloc(&d_h, B));
+    if (i_dev) d_i = iters; else CUC(cudaMalloc(&d_i, B));
+    CUC(cudaMalloc(&d_ex, ex.size()));
+    CUC(cudaMemcpy(d_ex, ex.data(), ex.size(), cudaMemcpyHostToDevice));
+    CUC(cudaMalloc(&d_err, sizeof(int)));
+    CUC(cudaMemset(d_err, 0, sizeof(int)));
+    const size_t per = qfs_form_scratch(n, p);
+    const size_t chunk = std::max<size_t>(1, std::min<size_t>(std::min<size_t>(B, 1184), ((size_t)1 << 30) / per));   // <= 8 CTAs per SM, <= 1 GB
+    CUC(cudaMalloc(&d_scratch, chunk * per));
+    for (size_t first = 0; first < B; first += chunk) {
+        const unsigned cnt = (unsigned)std::min(chunk, B - first);
+        k_form<<<cnt, QFS_FORM_NT>>>(d_c, d_ex, nterms, (int)B, (int)first, n, p, bound - 1, d_scratch, d_h, d_i, d_err);
+        CUC(cudaGetLastError());
+    }
     CUC(cudaMemcpy(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost));
     if (!h_dev) CUC(cudaMemcpy(heights, d_h, B, cudaMemcpyDeviceToHost));
     if (!i_dev) CUC(cudaMemcpy(iters, d_i, B, cudaMemcpyDeviceToHost));

@@ -116,7 +116,7 @@ def decode_height(h: int):
 
 def _check_engine_shape(p: int, n: int = NVARS):
     if n != NVARS:
-        raise DomainError(f"the GPU engine computes heights of quartics in 4 variables and of cubics in 3; got n={n}")
+        raise DomainError(f"the quartic engine computes heights of quartics in 4 variables (cubics: cubic.py, other n: forms.py); got n={n}")
     if p not in SUPPORTED_PRIMES:
         raise DomainError(f"p={p} is not supported by the GPU engine (supported: {SUPPORTED_PRIMES})")
 
@@ -230,8 +230,8 @@ def height_matrix(prob, algorithm: str = "wics", device: int = 0) -> HeightResul
     """
     if algorithm not in ("triv", "merge", "wics"):
         raise DomainError(f"unknown matrix algorithm {algorithm!r}")
-    if prob.n == 3:
-        return _cubic_height(prob, device)
+    if prob.n != NVARS:
+        return _other_n_height(prob, device)
     _check_engine_shape(prob.p, prob.n)
     c = coeff_vector(prob.f, prob.p)
     return height_of_coeffs(prob.p, c, prob.bound, device)
@@ -243,11 +243,21 @@ def height_naive(prob, device: int = 0) -> HeightResult:
     The reference keeps this driver as the independent check of height_matrix (same height, bound_used and
     iterations: tests/test_acceptance.py:128-138); here it is the matrix-free kernel of csrc/qfs_free.cuh.
     """
-    if prob.n == 3:
-        return _cubic_height(prob, device)
+    if prob.n != NVARS:
+        return _other_n_height(prob, device)
     _check_engine_shape(prob.p, prob.n)
     c = coeff_vector(prob.f, prob.p)
     return height_of_coeffs(prob.p, c, prob.bound, device, method="naive")
+
+
+def _other_n_height(prob, device: int = 0) -> HeightResult:
+    """n = 3: csrc/qfs_cubic.cuh; n = 2, 5, 6: csrc/qfs_form.cuh.  The operators are small there, so both drivers run the
+    matrix-free iteration; the results are the reference's (tests/golden/cubics.json, tests/golden/forms.json)."""
+    if prob.n == 3:
+        return _cubic_height(prob, device)
+    from .forms import form_height_batch, form_vector
+    hs, its = form_height_batch(prob.p, prob.n, form_vector(prob.f, prob.p, prob.n)[None, :], prob.bound, device)
+    return HeightResult(decode_height(hs[0]), int(prob.bound), int(its[0]))
 
 
 def _cubic_height(prob, device: int = 0) -> HeightResult:

@@ -115,8 +115,9 @@ def coeff_vector(f, p: int | None = None) -> np.ndarray:
 
 # ---- text formats --------------------------------------------------------------------------------
 
-def _parse_text_terms(text: str):
+def _parse_text_terms(text: str, nvars: int = NVARS):
     """[(exps, coeff)] from 'c*x1^a*x2^b + ...'; ParseError carries the offending position."""
+    NVARS = max(nvars, 4)   # the scanner keeps at least four exponent slots (callers of the 3-variable grammar slice them)
     n = len(text)
     i = 0
 
@@ -217,18 +218,17 @@ def _parse_compact_terms(text: str, nvars: int = NVARS):
 
 def parse_poly(text: str, nvars: int | None = NVARS, modulus: int | None = None) -> Quartic:
     """Parse either text format (auto-detected by ':') into a Quartic over F_modulus."""
-    if nvars not in (None, NVARS, 3):
-        raise DomainError(f"the GPU engine handles quartics in {NVARS} variables and cubics in 3, got nvars={nvars}")
+    if nvars is not None and not 2 <= nvars <= 6:
+        raise DomainError(f"the GPU engine handles forms of degree n in n = 2..6 variables, got nvars={nvars}")
     if modulus is None:
         raise DomainError("parse_poly needs the modulus p")
     if nvars is None and ":" not in text:
         # the reference infers the variable count from the highest variable that appears (polyring.py:438-520)
-        used = max((max((j + 1 for j, e in enumerate(exps) if e), default=0) for exps, _ in _parse_text_terms(text)), default=0)
-        if used == 3:
-            nvars = 3
-        elif used < 3:
-            raise DomainError(f"f has {used} variables; pass nvars (the GPU engine handles quartics in 4 variables and "
-                              f"cubics in 3), and f must be homogeneous of degree nvars (Calabi-Yau condition)")
+        used = max((max((j + 1 for j, e in enumerate(exps) if e), default=0) for exps, _ in _parse_text_terms(text, 6)), default=0)
+        if used < 2:
+            raise DomainError(f"f has {used} variables; f must be homogeneous of degree nvars in nvars >= 2 variables (Calabi-Yau condition)")
+        if used != NVARS:
+            nvars = used
     if nvars == 3:
         from .cubic import Cubic
         if ":" in text:
@@ -240,6 +240,17 @@ def parse_poly(text: str, nvars: int | None = NVARS, modulus: int | None = None)
                     raise ParseError("variable x4 exceeds nvars=3", 0)
                 terms.append((tuple(exps[:3]), c))
         return Cubic.from_terms(terms, modulus)
+    if nvars not in (None, NVARS):
+        from .forms import Form
+        if ":" in text:
+            terms = _parse_compact_terms(text, nvars)
+        else:
+            terms = []
+            for exps, c in _parse_text_terms(text, nvars):
+                if any(exps[nvars:]):
+                    raise ParseError(f"variable x{max(j + 1 for j, e in enumerate(exps) if e)} exceeds nvars={nvars}", 0)
+                terms.append((tuple(exps[:nvars]), c))
+        return Form.from_terms(terms, modulus, nvars)
     terms = _parse_compact_terms(text) if ":" in text else _parse_text_terms(text)
     return Quartic.from_terms(terms, modulus)
 
