@@ -113,7 +113,8 @@ struct DeltaMmaCfg {
     static constexpr int NWI = (P >= 11) ? QFS_DMMA_NWI11 : (P == 7 ? QFS_DMMA_NWI7 : (P == 5 ? QFS_DMMA_NWI5 : 4));  // item warps
     static constexpr int NTI = 32 * NWI;
     static constexpr int NT = NTI + 32;                          // + the store warp
-    static constexpr int SPLIT = (P >= 11) ? QFS_DMMA_SPLIT11 : 1;   // CTAs per quad
+    static constexpr int SPLIT = (P >= 11) ? QFS_DMMA_SPLIT11 : 1;   // CTAs per quad of a large launch
+    static constexpr int SPLIT_FEW = 16;                             // ... and when the launch has fewer quads than the GPU has SMs
     static constexpr int NBUF = (P >= 11) ? 2 : QFS_DMMA_NBUF;       // staging buffers (1: the copies of a phase overlap other CTAs' work only)
     static constexpr int SBW = (P >= 13) ? QFS_DMMA_SBW13 : (P >= 11 ? QFS_DMMA_SBW11 : (P == 7 ? QFS_DMMA_SBW7 : (P == 5 ? QFS_DMMA_SBW5 : 2048)));  // words per staging buffer
     static constexpr int SBX = S::d + 5;                         // window side: 4 zero cells below (taps reach t2, t3 <= 4), u = 0..d
@@ -200,7 +201,7 @@ struct DeltaPlan {
 };
 
 template <int P>
-inline bool delta_plan(DeltaPlan& plan)
+inline bool delta_plan(DeltaPlan& plan, int split = DeltaMmaCfg<P>::SPLIT)
 {
     using S = Shape<P>;
     using C = DeltaMmaCfg<P>;
@@ -271,18 +272,18 @@ inline bool delta_plan(DeltaPlan& plan)
         }
     }
     // parts of equal work (words), on phase boundaries
-    plan.parts.assign(C::SPLIT + 1, 0);
+    plan.parts.assign(split + 1, 0);
     uint64_t total = 0;
     for (const auto& ph : plan.phases) total += ph.nwords;
     uint64_t run = 0;
     int part = 1;
-    for (size_t i = 0; i < plan.phases.size() && part < C::SPLIT; ++i) {
+    for (size_t i = 0; i < plan.phases.size() && part < split; ++i) {
         run += plan.phases[i].nwords;
-        while (part < C::SPLIT && run * C::SPLIT >= total * part) plan.parts[part++] = (uint32_t)(i + 1);
+        while (part < split && run * split >= total * part) plan.parts[part++] = (uint32_t)(i + 1);
     }
-    for (; part <= C::SPLIT; ++part) plan.parts[part] = (uint32_t)plan.phases.size();
+    for (; part <= split; ++part) plan.parts[part] = (uint32_t)plan.phases.size();
     // blocks ((layer, group) runs of phases) and what to prefetch at their first phase, per part
-    for (int pt = 0; pt < C::SPLIT; ++pt) {
+    for (int pt = 0; pt < split; ++pt) {
         const uint32_t a = plan.parts[pt], b = plan.parts[pt + 1];
         for (uint32_t i = a; i < b; ++i) {
             DeltaPhase& ph = plan.phases[i];
@@ -454,7 +455,7 @@ template <int P>
 __global__ void __launch_bounds__(DeltaMmaCfg<P>::NT, DeltaMmaCfg<P>::MINB)
 k_delta_mma(const uint32_t* __restrict__ hbox_all, const uint8_t* __restrict__ A_all, const uint8_t* __restrict__ ecm_all,
             const DeltaPhase* __restrict__ phases, const DeltaPiece* __restrict__ pieces, const uint32_t* __restrict__ parts,
-            uint8_t* __restrict__ delta_all, int count)
+            uint8_t* __restrict__ delta_all, int count, int split)
 {
     using S = Shape<P>;
     using C = DeltaMmaCfg<P>;
@@ -466,7 +467,7 @@ k_delta_mma(const uint32_t* __restrict__ hbox_all, const uint8_t* __restrict__ A
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, tig = lane & 3;
-    const int quad = blockIdx.x / C::SPLIT, part = blockIdx.x % C::SPLIT;
+    const int quad = blockIdx.x / split, part = blockIdx.x % split;   // `split` CTAs per quad, each with its own part of the plan
     const int nlive = min(4, count - 4 * quad);   // slots >= count are padding: their Delta is zero
     const uint32_t pa = parts[part];
     const int nph = (int)(parts[part + 1] - pa);

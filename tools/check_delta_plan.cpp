@@ -14,12 +14,12 @@
 #include "../paper_2502_12428_b200/csrc/qfs_delta_mma.cuh"
 
 template <int P>
-int check()
+int check(int split = DeltaMmaCfg<P>::SPLIT)
 {
     using S = Shape<P>;
     using C = DeltaMmaCfg<P>;
     DeltaPlan plan;
-    if (!delta_plan<P>(plan)) { printf("p=%d: plan failed (SBW/MPTS too small)\n", P); return 1; }
+    if (!delta_plan<P>(plan, split)) { printf("p=%d: plan failed (SBW/MPTS too small)\n", P); return 1; }
     const int Lend = (S::Lg + 3) & ~3;
     std::vector<uint8_t> stored(Lend, 0), entry(Lend, 0);
     long tiles = 0, pts = 0, words = 0, blocks = 0;
@@ -101,9 +101,9 @@ int check()
         for (int I2 = 0; I1 + I2 <= S::D; ++I2)
             for (int I4 = 0; I1 + I2 + I4 <= S::D; ++I4)
                 if (!entry[S::gbase(I1, I2) + I4]) { bad("exponent missing", I1, I2, I4); break; }
-    for (int i = 0; i < C::SPLIT; ++i)
+    for (int i = 0; i < split; ++i)
         if (plan.parts[i] > plan.parts[i + 1]) bad("parts not monotone", i, 0, 0);
-    if (plan.parts[0] != 0 || plan.parts[C::SPLIT] != plan.phases.size()) bad("parts do not cover the phases", 0, 0, 0);
+    if (plan.parts[0] != 0 || plan.parts[split] != plan.phases.size()) bad("parts do not cover the phases", 0, 0, 0);
     printf("p=%d: %zu phases in %ld blocks, %zu pieces, %ld points in %ld tiles (%.1f%% of the tile rows), classes %d of %d, %ld staged words "
            "(%.2f x L), smem %d bytes: %s\n",
            P, plan.phases.size(), blocks, plan.pieces.size(), pts, tiles, 100.0 * pts / (16.0 * tiles), C::NCLS, C::NCLS_PAD, words,
@@ -119,5 +119,7 @@ int main()
     e += check<7>();
     e += check<11>();
     e += check<13>();
+    e += check<5>(DeltaMmaCfg<5>::SPLIT_FEW);   // the plan of launches with few quads
+    e += check<7>(DeltaMmaCfg<7>::SPLIT_FEW);
     return e ? 1 : 0;
 }
