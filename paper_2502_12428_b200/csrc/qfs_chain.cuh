@@ -47,6 +47,7 @@ k_chain(const uint8_t* __restrict__ M_all, const uint8_t* __restrict__ v0_all, c
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int NW = C::NT / 32;
     constexpr int NCH = S::pitch / 16;
+    constexpr int NCHR = (S::N + 15) / 16;   // 16-byte chunks of a row that hold a column: the pad chunks behind them are not read
 
     while (true) {
         if (tid == 0) s_slot = atomicAdd(queue, 1);
@@ -71,11 +72,11 @@ k_chain(const uint8_t* __restrict__ M_all, const uint8_t* __restrict__ v0_all, c
             const uint4* src = reinterpret_cast<const uint4*>(v0_all + (size_t)slot * S::pitch);
             for (int i = tid; i < NCH; i += C::NT) {
                 uint4 x = src[i];
-                if (i == NCH - 1 && S::pitch != S::N) {  // the pad bytes of v1 are never written by the builder: mask them
+                if (16 * i + 16 > S::N) {  // the pad bytes of v1 (and of M's rows) are never written by the builder: mask every chunk past N
                     uint32_t w[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
                     for (int b = 0; b < 16; ++b)
-                        if (16 * (NCH - 1) + b >= S::N) w[b >> 2] &= ~(0xFFu << (8 * (b & 3)));
+                        if (16 * i + b >= S::N) w[b >> 2] &= ~(0xFFu << (8 * (b & 3)));
                     x = make_uint4(w[0], w[1], w[2], w[3]);
                 }
                 reinterpret_cast<uint4*>(va)[i] = x;
@@ -89,7 +90,7 @@ k_chain(const uint8_t* __restrict__ M_all, const uint8_t* __restrict__ v0_all, c
                 uint32_t acc[C::UNROLL];
 #pragma unroll
                 for (int u = 0; u < C::UNROLL; ++u) acc[u] = 0;
-                for (int ch = lane; ch < NCH; ch += 32) {
+                for (int ch = lane; ch < NCHR; ch += 32) {
                     const uint4 v = reinterpret_cast<const uint4*>(va)[ch];
                     uint4 m[C::UNROLL];
 #pragma unroll
@@ -171,6 +172,7 @@ k_chain_grid(const uint8_t* __restrict__ M_all, const uint8_t* __restrict__ v0_a
     // consecutive rows go to different CTAs: every SM streams the same number of rows (+-1)
     const int gw = (tid >> 5) * gridDim.x + blockIdx.x, GW = gridDim.x * (C::NT / 32);
     constexpr int NCH = S::pitch / 16;
+    constexpr int NCHR = (S::N + 15) / 16;   // 16-byte chunks of a row that hold a column: the pad chunks behind them are not read
 
     for (int i = tid; i < count; i += C::NT) sflag[i] = start_it > 0 ? v0_all[(size_t)i * S::pitch + S::cap] : 0;
     __syncthreads();
@@ -208,7 +210,7 @@ k_chain_grid(const uint8_t* __restrict__ M_all, const uint8_t* __restrict__ v0_a
                 const uint4* mrow = reinterpret_cast<const uint4*>(M + (size_t)row * S::pitch);
                 uint32_t acc = 0;
                 int ch0 = 0;
-                for (; ch0 + 32 * C::KCH <= NCH; ch0 += 32 * C::KCH) {
+                for (; ch0 + 32 * C::KCH <= NCHR; ch0 += 32 * C::KCH) {
                     uint4 m[C::KCH];
 #pragma unroll
                     for (int k = 0; k < C::KCH; ++k) m[k] = ld_stream16(mrow + ch0 + 32 * k + lane);
@@ -221,7 +223,7 @@ k_chain_grid(const uint8_t* __restrict__ M_all, const uint8_t* __restrict__ v0_a
                         acc = __dp4a(m[k].w, v.w, acc);
                     }
                 }
-                for (int ch = ch0 + lane; ch < NCH; ch += 32) {
+                for (int ch = ch0 + lane; ch < NCHR; ch += 32) {
                     const uint4 m = ld_stream16(mrow + ch);
                     const uint4 v = reinterpret_cast<const uint4*>(sv)[ch];
                     acc = __dp4a(m.x, v.x, acc);

@@ -265,9 +265,13 @@ int build_tables(qfs_ctx* ctx)
                 while (ga < gend) {
                     PanelItem it{}, best{};
                     int best_st = -1, gb = ga;
-                    while (gb < SC::NGRP) {
-                        int nb = std::min(SC::NGRP, gb + SC::LINEG);
-                        if (nb >= gend) nb = SC::NGRP;
+                    // the rows are written up to the end of the 32-byte sector that holds the last column; the pad columns beyond it
+                    // (pitch = N rounded up to 128) stay unwritten: nothing reads them (k_chain / k_chain_grid mask the vector's pad
+                    // and stop at that sector, the taps and exports copy N columns)
+                    constexpr int NGRPW = ((S::N + 31) / 32 * 32) / CPG;
+                    while (gb < NGRPW) {
+                        int nb = std::min(NGRPW, gb + SC::LINEG);
+                        if (nb >= gend) nb = NGRPW;
                         if (nb - ga > SC::MAXG) break;
                         const int st = make(ga, nb, it);
                         if (st > budget && best_st >= 0) break;
