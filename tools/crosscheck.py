@@ -31,10 +31,15 @@ done = 0
 w = 0
 while done < a.count:
     n = min(a.block, a.count - done)
-    c = q.sample_block(a.p, n, a.seed, w)
-    t0 = time.perf_counter(); hm, im = eng.heights(c, 10); t1 = time.perf_counter()
-    hf, jf = eng.heights(c, 10, matrix_free=True); t2 = time.perf_counter()
+    import torch
+    c = torch.empty((n, 35), dtype=torch.uint8, device="cuda:0")
+    _, clean = eng.sample(a.seed, w, n, out=c)          # the reference's seeded stream, drawn on the device
+    if not clean:
+        c = torch.from_numpy(q.sample_block(a.p, n, a.seed, w)).cuda()
+    t0 = time.perf_counter(); hm, im = eng.heights(c, 10); torch.cuda.synchronize(); t1 = time.perf_counter()
+    hf, jf = eng.heights(c, 10, matrix_free=True); torch.cuda.synchronize(); t2 = time.perf_counter()
     t_m += t1 - t0; t_f += t2 - t1
+    hm, im, hf, jf = (x.cpu().numpy() for x in (hm, im, hf, jf))
     mism += int((hm != hf).sum() + (im != jf).sum())
     hist += np.bincount(hm.astype(np.int64), minlength=12)[:12]
     done += n; w += 1

@@ -28,5 +28,12 @@ rng = np.random.default_rng(5)
 for p in (3, 5, 13):
     hs, its = q.cubic_height_batch(p, rng.integers(1, p, size=(40, 10)).astype(np.uint8), 5)
     print("cubic", p, np.bincount(hs.astype(np.int64)).tolist(), flush=True)
+for n, p in ((2, 5), (5, 3), (6, 3)):
+    from paper_2502_12428_b200.forms import exponents
+    hs, its = q.form_height_batch(p, n, rng.integers(1, p, size=(6, len(exponents(n)))).astype(np.uint8), 3)
+    print("form", n, p, np.bincount(hs.astype(np.int64)).tolist(), flush=True)
+got, clean = get_engine(5, 0).sample(1, 2, 5000)
+assert clean and np.array_equal(got, q.sample_block(5, 5000, 1, 2))
+print("sampler ok", flush=True)
 if os.environ.get("QFS_DELTA_DIRECT"):
     print("k_delta_direct was used for Delta")
