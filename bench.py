@@ -103,9 +103,27 @@ def measured_traffic(p, kernel, hard, launches):
         return None
 
 
+_SAMPLER_SRC = r"""
+import sys, time
+import pynvml as n
+n.nvmlInit()
+uuid = sys.argv[1]
+try:
+    h = n.nvmlDeviceGetHandleByUUID(uuid.encode()) if uuid != "-" else n.nvmlDeviceGetHandleByIndex(int(sys.argv[2]))
+except Exception:
+    h = n.nvmlDeviceGetHandleByIndex(int(sys.argv[2]))
+get = getattr(n, "nvmlDeviceGetCurrentClocksEventReasons", None) or n.nvmlDeviceGetCurrentClocksThrottleReasons
+print("max", n.nvmlDeviceGetMaxClockInfo(h, n.NVML_CLOCK_SM), flush=True)
+while True:
+    print(time.time(), n.nvmlDeviceGetClockInfo(h, n.NVML_CLOCK_SM), int(get(h)), flush=True)
+    time.sleep(0.004)
+"""
+
+
 class ClockSampler:
-    """SM clock and clock-event (throttle) reasons sampled through NVML every ~10 ms while the timed region runs (a timed
-    region is 50-100 ms: nvidia-smi's own loop is too coarse for it); falls back to `nvidia-smi -lms` if NVML cannot be loaded."""
+    """SM clock and clock-event (throttle) reasons sampled through NVML every ~5 ms by a SEPARATE process (a sampling thread in
+    this process starves while the benchmark's Python thread runs); start() early, then window(t0, t1) keeps the samples whose
+    wall-clock stamp lies inside the timed region.  Falls back to `nvidia-smi -lms` if NVML cannot be loaded."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -117,75 +135,64 @@ class ClockSampler:
         self.index = index
         self.lines = []
         self.proc = None
-        self.nvml = None
-        self.samples = []
-        self.mask = 0
-        self.max_mhz = None
-        self._stop = threading.Event()
-
-    def _nvml_handle(self):
-        import pynvml
-        pynvml.nvmlInit()
-        try:
-            import torch
-            uuid = str(torch.cuda.get_device_properties(self.index).uuid)
-            return pynvml, pynvml.nvmlDeviceGetHandleByUUID(("GPU-" + uuid).encode())
-        except Exception:
-            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
+        self.mode = None
 
     def start(self):
         try:
-            self.nvml, self.handle = self._nvml_handle()
-            self.max_mhz = float(self.nvml.nvmlDeviceGetMaxClockInfo(self.handle, self.nvml.NVML_CLOCK_SM))
-            self.thread = threading.Thread(target=self._poll, daemon=True)
-            self.thread.start()
-            return
+            import pynvml  # noqa: F401  (the child needs it)
+            try:
+                import torch
+                uuid = "GPU-" + str(torch.cuda.get_device_properties(self.index).uuid)
+            except Exception:
+                uuid = "-"
+            self.proc = subprocess.Popen([sys.executable, "-c", _SAMPLER_SRC, uuid, str(self.index)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.mode = "nvml"
         except Exception:
-            self.nvml = None
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "200"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            try:
+                self.proc = subprocess.Popen(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "100"],
+                    stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                self.mode = "smi"
+            except Exception:
+                self.proc = None
+        if self.proc:
             self.thread = threading.Thread(target=self._pump, daemon=True)
             self.thread.start()
-        except Exception:
-            self.proc = None
-
-    def _poll(self):
-        n = self.nvml
-        while not self._stop.is_set():
-            try:
-                self.samples.append(float(n.nvmlDeviceGetClockInfo(self.handle, n.NVML_CLOCK_SM)))
-                get = getattr(n, "nvmlDeviceGetCurrentClocksEventReasons", None) or n.nvmlDeviceGetCurrentClocksThrottleReasons
-                self.mask |= int(get(self.handle))
-            except Exception:
-                pass
-            time.sleep(0.01)
+            time.sleep(0.5)   # the child imports and initialises NVML before the timed region starts
 
     def _pump(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
 
-    def stop(self):
-        if self.nvml is not None:
-            self._stop.set()
-            self.thread.join(timeout=1)
-            sm = self.samples
-            return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": self.max_mhz, "samples": len(sm),
-                    "reasons": sorted(nm for bit, nm in self.BITS.items() if self.mask & bit), "source": "nvml, 10 ms period"}
+    def stop(self, t0=None, t1=None):
         if not self.proc:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.25)
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no clock sampler available"]}
+        time.sleep(0.05)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=2)
         except Exception:
             self.proc.kill()
+        if self.mode == "nvml":
+            mx, sm, mask = None, [], 0
+            for _, ln in self.lines:
+                f = ln.split()
+                if len(f) == 2 and f[0] == "max":
+                    mx = float(f[1])
+                elif len(f) == 3:
+                    t = float(f[0])
+                    if (t0 is None or t >= t0) and (t1 is None or t <= t1):
+                        sm.append(float(f[1]))
+                        mask |= int(f[2])
+            return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "samples": len(sm),
+                    "reasons": sorted(nm for bit, nm in self.BITS.items() if mask & bit),
+                    "source": "nvml in a sampler process, ~5 ms period, samples stamped inside the timed regions"}
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for t, ln in self.lines:
             f = [x.strip() for x in ln.split(",")]
-            if len(f) < 7:
+            if len(f) < 7 or (t0 is not None and t < t0) or (t1 is not None and t > t1 + 0.2):
                 continue
             try:
                 sm.append(float(f[0]))
@@ -196,7 +203,7 @@ class ClockSampler:
                 if val.lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
-                "samples": len(sm), "reasons": sorted(reasons), "source": "nvidia-smi -lms 200"}
+                "samples": len(sm), "reasons": sorted(reasons), "source": "nvidia-smi -lms 100"}
 
 
 def algorithmic_bytes(p, iters_hard):
@@ -287,14 +294,15 @@ def measure_gpu(p, batch, steps, warmup, seed, rank, world, device, dist):
             dist.barrier()
         torch.cuda.synchronize(device)
 
+    sampler = ClockSampler(device)
+    sampler.start()
     for _ in range(warmup):
         eng.heights(dev, 10, out=(hs, its))
     stage = {"ms_power": 0.0, "ms_delta": 0.0, "ms_matrix": 0.0, "ms_matvec": 0.0, "ms_total": 0.0}
     launches = 0
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    sampler = ClockSampler(device)
-    sampler.start()
+    wall0 = time.time()
     e0.record()
     for _ in range(steps):
         eng.heights(dev, 10, out=(hs, its))
@@ -321,7 +329,7 @@ def measure_gpu(p, batch, steps, warmup, seed, rank, world, device, dist):
         height_batch(p, h_in, 10, devices=[device], out=(h_hs, h_its))
     torch.cuda.synchronize(device)
     e2e_s = time.perf_counter() - t0
-    clocks = sampler.stop()
+    clocks = sampler.stop(wall0, time.time())
 
     heights = hs.cpu().numpy()
     iters = its.cpu().numpy()
