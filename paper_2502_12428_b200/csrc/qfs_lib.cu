@@ -595,7 +595,8 @@ int run_heights(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, int bound, int8_t
 
     // pass 1: Fedder test for every surface (height 1 or pending)
     CU(cudaEventRecord(ctx->ev[0], ctx->stream));
-    k_fedder<P><<<(unsigned)((B + PowerCfg<P>::FED_WARPS - 1) / PowerCfg<P>::FED_WARPS), PowerCfg<P>::FED_WARPS * 32,
+    constexpr int FED_SPC = PowerCfg<P>::FED_WARPS / PowerCfg<P>::FED_WPS;   // surfaces per CTA
+    k_fedder<P><<<(unsigned)((B + FED_SPC - 1) / FED_SPC), PowerCfg<P>::FED_WARPS * 32,
                   PowerCfg<P>::FED_SMEM, ctx->stream>>>(d_coeffs, (int)B, ctx->unrank.as<uint32_t>(), d_heights, d_flags);
     ctx->stats.kernel_launches++;
     CU(cudaGetLastError());

@@ -48,7 +48,8 @@ template <int P>
 struct PowerCfg {
     using S = Shape<P>;
     static constexpr int J0 = (P - 1) / 2;              // last fully computed level of the Fedder chain
-    static constexpr int FED_WARPS = (P >= 13) ? 4 : 8;  // surfaces per CTA in k_fedder (shared-memory bound at p = 13)
+    static constexpr int FED_WPS = (P >= 11) ? 4 : 1;    // warps that share one surface (and one cube) in k_fedder
+    static constexpr int FED_WARPS = (P >= 11) ? 4 : 8;  // warps per CTA in k_fedder: FED_WARPS / FED_WPS surfaces per CTA
     static constexpr int FED_BUF = qround16(qc3(4 * J0 + 3));
     static constexpr int RB_DEG = 4 * P;                // row-base tables up to this degree
     static constexpr int FULL_NT = 256;
@@ -63,7 +64,7 @@ struct PowerCfg {
     static constexpr int FED_BOX = (J0 > 1) ? qround16(FED_SB * FED_SB * FED_SB) : 0;
     static constexpr int FULL_SB = 4 * P + 5;
     static constexpr int FULL_BOX = qround16(FULL_SB * FULL_SB * FULL_SB);
-    static constexpr int FED_SMEM = FED_WARPS * (2 * FED_BUF + FED_BOX) + 2 * FED_RB;
+    static constexpr int FED_SMEM = (FED_WARPS / FED_WPS) * (2 * FED_BUF + FED_BOX) + 2 * FED_RB;
     static constexpr int FULL_SMEM = FULL_BUF + FULL_BOX;
 };
 
@@ -149,118 +150,90 @@ __device__ __forceinline__ void lex_to_box(const uint8_t* __restrict__ lex, uint
 }
 
 // ---------------------------------------------------------------------------------------------
+// Fedder test: height 1 iff the coefficient of (x1 x2 x3 x4)^(p-1) in f^(p-1) is nonzero (polyring.py:316-332).
+// p - 1 = 2 J0, so that coefficient is a single dot product of F = f^J0 with its own reflection,
+//     [f^(p-1)]_cap = sum_K F[K] * F[cap - K],     K in basis(4 J0) with every K_i <= p-1,
+// and only the levels f^2 .. f^J0 are ever computed (box form: coefficients of f in registers, compile-time tap offsets).
+// A group of WPS warps works on one surface: one warp for p <= 7 (FED_WARPS surfaces per CTA), the whole four-warp CTA for
+// p >= 11, where the cube of the box form (15.6 / 24.4 KB) would otherwise leave room for 8 / 4 warps per SM.
 template <int P>
 __global__ void __launch_bounds__(PowerCfg<P>::FED_WARPS * 32)
 k_fedder(const uint8_t* __restrict__ coeffs, int count, const uint32_t* __restrict__ unrank,
          int8_t* __restrict__ heights, int* __restrict__ err)
 {
     using C = PowerCfg<P>;
+    constexpr int WPS = C::FED_WPS, GT = 32 * WPS;     // warps / threads per surface
+    constexpr int SPC = C::FED_WARPS / WPS;            // surfaces per CTA
     extern __shared__ __align__(16) uint8_t smem[];
-    uint16_t* rb = reinterpret_cast<uint16_t*>(smem + C::FED_WARPS * (2 * C::FED_BUF + C::FED_BOX));
-    __shared__ uint32_t s_terms[C::FED_WARPS][36];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint16_t* rb = reinterpret_cast<uint16_t*>(smem + SPC * (2 * C::FED_BUF + C::FED_BOX));
+    __shared__ int s_dot[SPC];
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int grp = tid / GT, gt = tid - grp * GT;     // surface of the CTA, thread inside its group
+    auto gsync = [&]() { if (WPS == 1) __syncwarp(); else __syncthreads(); };   // WPS > 1: one surface per CTA
+    static_assert(WPS == 1 || SPC == 1, "several warps per surface: one surface per CTA");
     fill_rb_tables<P>(rb, 4 * C::J0, tid, C::FED_WARPS * 32);
+    if (tid < SPC) s_dot[tid] = 0;
     __syncthreads();
 
-    const int sid = blockIdx.x * C::FED_WARPS + warp;
-    if (sid >= count) return;
+    const int sid = blockIdx.x * SPC + grp;
+    if (sid >= count) return;                          // whole groups leave together (WPS > 1: the whole CTA)
     const uint8_t* cf = coeffs + (size_t)35 * sid;
-    uint8_t* bufA = smem + (size_t)warp * (2 * C::FED_BUF + C::FED_BOX);
+    uint8_t* bufA = smem + (size_t)grp * (2 * C::FED_BUF + C::FED_BOX);
     uint8_t* bufB = bufA + C::FED_BUF;
-    uint8_t* box = bufB + C::FED_BUF;  // cube of the box-form products (full levels)
-    uint32_t* terms = s_terms[warp];
+    uint8_t* box = bufB + C::FED_BUF;  // cube of the box-form products
     if (C::J0 > 1)
-        for (int i = lane; i < C::FED_BOX / 16; i += 32) reinterpret_cast<uint4*>(box)[i] = make_uint4(0, 0, 0, 0);
+        for (int i = gt; i < C::FED_BOX / 16; i += GT) reinterpret_cast<uint4*>(box)[i] = make_uint4(0, 0, 0, 0);
 
-    // nonzero terms of f via warp ballot; lanes 0..31 hold coefficients 0..31, lanes 0..2 also 32..34
-    const uint32_t* unrank4 = unrank + qunrank_offset(1);
-    int nf = 0;
-    {
+    // input checks (residues < p, not the zero form) by the group's first warp; every thread keeps the 35 coefficients
+    if (gt < 32) {
         const uint32_t c0 = cf[lane];
         const uint32_t c1 = lane < 3 ? cf[32 + lane] : 0;
         const bool bad = (c0 >= (uint32_t)P) || (c1 >= (uint32_t)P);
         const unsigned badm = __ballot_sync(0xffffffffu, bad);
-        const unsigned m0 = __ballot_sync(0xffffffffu, c0 != 0 && c0 < (uint32_t)P);
-        const unsigned m1 = __ballot_sync(0xffffffffu, c1 != 0 && c1 < (uint32_t)P);
-        if (lane == 0 && (badm || !(m0 | m1))) atomicOr(err, QFS_ERRBIT_INPUT);
+        const unsigned any = __ballot_sync(0xffffffffu, (c0 != 0 && c0 < (uint32_t)P) || (c1 != 0 && c1 < (uint32_t)P));
+        if (lane == 0 && (badm || !any)) atomicOr(err, QFS_ERRBIT_INPUT);
         bufA[lane] = (uint8_t)(c0 < (uint32_t)P ? c0 : 0);
         if (lane < 3) bufA[32 + lane] = (uint8_t)(c1 < (uint32_t)P ? c1 : 0);
-        if (m0 >> lane & 1) {
-            const uint32_t mm = unrank4[lane];
-            const uint32_t j1 = mm & 255, j2 = (mm >> 8) & 255, j3 = mm >> 16;
-            terms[__popc(m0 & ((1u << lane) - 1))] = j1 | (j2 << 4) | (j3 << 8) | ((4 - j1 - j2 - j3) << 12) | (c0 << 16);
-        }
-        const int n0 = __popc(m0);
-        if (lane < 3 && (m1 >> lane & 1)) {
-            const uint32_t mm = unrank4[32 + lane];
-            const uint32_t j1 = mm & 255, j2 = (mm >> 8) & 255, j3 = mm >> 16;
-            terms[n0 + __popc(m1 & ((1u << lane) - 1))] = j1 | (j2 << 4) | (j3 << 8) | ((4 - j1 - j2 - j3) << 12) | (c1 << 16);
-        }
-        nf = n0 + __popc(m1);
     }
-    __syncwarp();
+    gsync();
 
     uint8_t* cur = bufA;
     uint8_t* nxt = bufB;
-    // full levels f^2 .. f^J0 in box form (coefficients of f in registers, zero where f has no term)
+    // levels f^2 .. f^J0 in box form
     if (C::J0 > 1) {
         uint32_t c[35];
 #pragma unroll
         for (int t = 0; t < 35; ++t) c[t] = cur[t];
 #pragma unroll 1
         for (int j = 2; j <= C::J0; ++j) {
-            lex_to_box<C::FED_SB>(cur, box, 4 * (j - 1), unrank + qunrank_offset(j - 1), lane, 32);
-            __syncwarp();
-            mul_by_f_box<P, C::FED_SB>(box, nxt, 4 * j, unrank + qunrank_offset(j), c, lane, 32);
-            __syncwarp();
+            lex_to_box<C::FED_SB>(cur, box, 4 * (j - 1), unrank + qunrank_offset(j - 1), gt, GT);
+            gsync();
+            mul_by_f_box<P, C::FED_SB>(box, nxt, 4 * j, unrank + qunrank_offset(j), c, gt, GT);
+            gsync();
             uint8_t* t = cur; cur = nxt; nxt = t;
         }
     }
-    // transition level j = J0+1:  R_j[K] = sum_J f[J] * F_J0[cap - K - J],  K in basis(dk), dk = 4(p-2-J0)
+    // the dot product of F = f^J0 with its reflection about cap = (p-1, p-1, p-1, p-1)
     {
-        constexpr int dk = 4 * (P - 2 - C::J0);
-        constexpr int nk = qc3(dk + 3);
-        constexpr int din = 4 * C::J0;
-        const uint16_t* rbi = rb + C::rb_offset(din);
-        const uint32_t* un = unrank + qunrank_offset(dk / 4);  // unused when dk == 0
-        for (int o = lane; o < nk; o += 32) {
-            int k1 = 0, k2 = 0, k3 = 0;
-            if (dk > 0) { const uint32_t m = un[o]; k1 = m & 255; k2 = (m >> 8) & 255; k3 = m >> 16; }
-            const int k4 = dk - k1 - k2 - k3;
-            uint32_t acc = 0;
-            for (int t = 0; t < nf; ++t) {
-                const uint32_t tm = terms[t];
-                const int a1 = P - 1 - k1 - (int)(tm & 15), a2 = P - 1 - k2 - (int)((tm >> 4) & 15);
-                const int a3 = P - 1 - k3 - (int)((tm >> 8) & 15), a4 = P - 1 - k4 - (int)((tm >> 12) & 15);
-                if ((a1 | a2 | a3 | a4) >= 0) acc += (tm >> 16) * cur[rbi[a1 * (din + 1) + a2] + a3];
-            }
-            nxt[o] = (uint8_t)(acc % (uint32_t)P);
+        constexpr int dF = 4 * C::J0, nF = qc3(dF + 3);
+        const uint16_t* rbi = rb + C::rb_offset(dF);
+        const uint32_t* un = unrank + qunrank_offset(C::J0);
+        uint32_t acc = 0;
+        for (int o = gt; o < nF; o += GT) {
+            const uint32_t m = un[o];
+            const int k1 = m & 255, k2 = (m >> 8) & 255, k3 = m >> 16, k4 = dF - k1 - k2 - k3;
+            if (k1 < P && k2 < P && k3 < P && k4 < P)
+                acc += (uint32_t)cur[o] * cur[rbi[(P - 1 - k1) * (dF + 1) + (P - 1 - k2)] + (P - 1 - k3)];
         }
-        __syncwarp();
-        uint8_t* t = cur; cur = nxt; nxt = t;
-    }
-    // restricted levels j = J0+2 .. p-1:  R_j[K] = sum_J f[J] * R_{j-1}[K + J]
-#pragma unroll 1
-    for (int j = C::J0 + 2; j <= P - 1; ++j) {
-        const int dk = 4 * (P - 1 - j);
-        const int nk = qc3(dk + 3);
-        const int din = dk + 4;
-        const uint16_t* rbi = rb + C::rb_offset(din);
-        const uint32_t* un = unrank + qunrank_offset(dk > 0 ? dk / 4 : 1);
-        for (int o = lane; o < nk; o += 32) {
-            int k1 = 0, k2 = 0, k3 = 0;
-            if (dk > 0) { const uint32_t m = un[o]; k1 = m & 255; k2 = (m >> 8) & 255; k3 = m >> 16; }
-            uint32_t acc = 0;
-            for (int t = 0; t < nf; ++t) {
-                const uint32_t tm = terms[t];
-                acc += (tm >> 16) * cur[rbi[(k1 + (int)(tm & 15)) * (din + 1) + k2 + (int)((tm >> 4) & 15)] + k3 + (int)((tm >> 8) & 15)];
-            }
-            nxt[o] = (uint8_t)(acc % (uint32_t)P);
+        acc = __reduce_add_sync(0xffffffffu, acc % (uint32_t)P);
+        if (WPS == 1) {
+            if (lane == 0) heights[sid] = (acc % (uint32_t)P) ? (int8_t)1 : (int8_t)-1;
+        } else {
+            if (lane == 0) atomicAdd(&s_dot[grp], (int)(acc % (uint32_t)P));
+            __syncthreads();
+            if (gt == 0) heights[sid] = (s_dot[grp] % P) ? (int8_t)1 : (int8_t)-1;
         }
-        __syncwarp();
-        uint8_t* t = cur; cur = nxt; nxt = t;
     }
-    if (lane == 0) heights[sid] = cur[0] ? (int8_t)1 : (int8_t)-1;
 }
 
 // ---------------------------------------------------------------------------------------------

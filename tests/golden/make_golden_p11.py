@@ -1,5 +1,5 @@
 #!/usr/bin/env python3
-"""F_11 stage goldens from the UNMODIFIED reference package (qfsplit): minutes and GBs per surface.
+"""F_11 (and, with GOLDEN_P=13, F_13) stage goldens from the UNMODIFIED reference package (qfsplit): minutes and GBs per surface.
 
 Run in the authoring container only (the GPU box has no /root/reference):
 
@@ -27,9 +27,11 @@ sys.path.insert(0, HERE)
 
 from make_golden import coeff_vector, dense_of  # noqa: E402
 
-P = 11
-ROWS = (0, 1, 12341 // 3, 12341 // 2, 12340)
+P = int(os.environ.get("GOLDEN_P", "11"))          # 11 (default) or 13: GOLDEN_P=13 python tests/golden/make_golden_p11.py 2
+NN = math.comb(4 * (P - 1) + 3, 3)                # 12341 / 20825
+ROWS = (0, 1, NN // 3, NN // 2, NN - 1)
 STRIDE = 997
+NSEED = 4 if P == 11 else 2                       # seeded hard surfaces beside the published rows
 
 
 def _one(job):
@@ -70,7 +72,7 @@ def _one(job):
     rec["height"] = np.int64(height)
     rec["iters"] = np.int64(iters)
     rec["seconds"] = np.float64(time.time() - t0)
-    np.savez_compressed(os.path.join(HERE, f"_p11_part_{tag}.npz"), **rec)
+    np.savez_compressed(os.path.join(HERE, f"_p{P}_part_{tag}.npz"), **rec)
     print(tag, "height", height, "iters", iters, "%.0f s" % (time.time() - t0), flush=True)
     return tag
 
@@ -87,23 +89,23 @@ def main():
     rng = np.random.default_rng([0, 0])
     k = 0
     idx = 0
-    while k < 4:
+    while k < NSEED:
         f = sample_surface(rng, P)
         if not fedder_survives(power_mod_p(f, P - 1)):
             jobs.append((f"seed0_i{idx}", coeff_vector(f).tolist()))
             k += 1
         idx += 1
-    todo = [j for j in jobs if not os.path.exists(os.path.join(HERE, f"_p11_part_{j[0]}.npz"))]
+    todo = [j for j in jobs if not os.path.exists(os.path.join(HERE, f"_p{P}_part_{j[0]}.npz"))]
     print("jobs", [j[0] for j in jobs], "todo", len(todo), flush=True)
     with ProcessPoolExecutor(max_workers=jobs_n) as pool:
         list(pool.map(_one, todo))
     flat = {"p": np.int64(P), "count": np.int64(len(jobs)), "tags": np.array([j[0] for j in jobs])}
     for i, (tag, _) in enumerate(jobs):
-        part = np.load(os.path.join(HERE, f"_p11_part_{tag}.npz"))
+        part = np.load(os.path.join(HERE, f"_p{P}_part_{tag}.npz"))
         for key in part.files:
             flat[f"s{i}_{key}"] = part[key]
-    np.savez_compressed(os.path.join(HERE, "stages_p11.npz"), **flat)
-    print("stages_p11.npz", len(jobs), "surfaces")
+    np.savez_compressed(os.path.join(HERE, f"stages_p{P}.npz"), **flat)
+    print(f"stages_p{P}.npz", len(jobs), "surfaces")
 
 
 if __name__ == "__main__":
