@@ -144,30 +144,36 @@ def test_bound_semantics(bound):
     assert np.array_equal(hs, ohs) and np.array_equal(its, oits)
 
 
-# ---- F_11: the reference's own intermediates (tests/golden/make_golden_p11.py; ~5 CPU-minutes per surface) ----------------
-def _p11():
-    z = np.load(os.path.join(GOLDEN, "stages_p11.npz"))
+# ---- F_11, F_13: the reference's own intermediates (tests/golden/make_golden_p11.py; ~5 resp. ~25 CPU-minutes per surface) ----------
+def _pbig(p):
+    path = os.path.join(GOLDEN, f"stages_p{p}.npz")
+    if not os.path.exists(path):
+        pytest.skip(f"stages_p{p}.npz not generated")
+    z = np.load(path)
     return z, int(z["count"])
 
 
-def test_f11_stage_power_golden():
-    z, n = _p11()
+@pytest.mark.parametrize("p", [11, 13])
+def test_big_prime_stage_power_golden(p):
+    z, n = _pbig(p)
     coeffs = np.stack([z[f"s{i}_coeffs"] for i in range(n)])
-    g, fed = _engine(11).stage_power(coeffs)
+    g, fed = _engine(p).stage_power(coeffs)
     for i in range(n):
         assert np.array_equal(g[i], z[f"s{i}_g"]), f"g mismatch surface {i}"
         assert not fed[i]
 
 
-def test_f11_delta_matrix_chain_golden():
-    """Delta (sha256 of the dense 14 391 741-entry vector + every 997th entry), M (sha256 of the 12341 x 12341 operator + five
-    rows) and the whole matvec trace, heights and iteration counts of eight F_11 surfaces against what the reference
-    computed (extended suite of the reference, tests/test_acceptance.py:84-89; tests/test_mtsmatrix.py:174-198)."""
-    z, n = _p11()
-    eng = _engine(11)
+@pytest.mark.parametrize("p", [11, 13])
+def test_big_prime_delta_matrix_chain_golden(p):
+    """Delta (sha256 of the dense vector -- 14 391 741 entries at p = 11, 40 885 625 at p = 13 -- and every 997th entry), M (sha256
+    of the 12341^2 resp. 20825^2 operator and five rows) and the whole matvec trace, heights and iteration counts against what the
+    reference computed (extended suite of the reference, tests/test_acceptance.py:84-89; tests/test_mtsmatrix.py:174-198)."""
+    z, n = _pbig(p)
+    eng = _engine(p)
     coeffs = np.stack([z[f"s{i}_coeffs"] for i in range(n)])
-    for lo in range(0, n, 2):        # two surfaces at a time: 2 x 152 MB of M on the host
-        sel = list(range(lo, min(n, lo + 2)))
+    step = 2 if p == 11 else 1        # surfaces at a time: 152 MB resp. 434 MB of M each on the host
+    for lo in range(0, n, step):
+        sel = list(range(lo, min(n, lo + step)))
         dl = eng.stage_delta(coeffs[sel])
         for k, i in enumerate(sel):
             assert np.array_equal(dl[k][::997], z[f"s{i}_delta_every"]), f"Delta sample mismatch surface {i}"
