@@ -30,7 +30,7 @@
 // Pipeline.  NWI item warps + one store warp, NBUF staging buffers with full/empty mbarriers: an item warp that has finished its
 // share of phase i arrives on full[i % NBUF]; the store warp waits for full, issues the phase's bulk copies (a piece per lane),
 // waits until they have read shared memory and arrives on empty.  There is no barrier among the item warps: the full/empty
-// handshake bounds their lag to one phase, the window has RING = 6 planes and the class rows 3 buffers, so the next layer's
+// handshake bounds their lag to NBUF - 1 phases, the window has 5 + lag planes and the class rows 2 + lag buffers, so the next layer's
 // plane and the next group's rows are prefetched a block ahead (cp.async.bulk global -> shared, mbarrier complete_tx) into slots
 // no lagging warp still reads, and every warp derives the same mbarrier parities from the phase list.
 //
@@ -89,13 +89,16 @@ struct DeltaPiece {
 #define QFS_DMMA_NWI7 4
 #endif
 #ifndef QFS_DMMA_NWI11
-#define QFS_DMMA_NWI11 16
+#define QFS_DMMA_NWI11 8
 #endif
 #ifndef QFS_DMMA_MAXB
 #define QFS_DMMA_MAXB 4
 #endif
 #ifndef QFS_DMMA_NBUF
 #define QFS_DMMA_NBUF 1
+#endif
+#ifndef QFS_DMMA_NBUF11
+#define QFS_DMMA_NBUF11 2
 #endif
 #ifndef QFS_DMMA_SPLIT11
 #define QFS_DMMA_SPLIT11 16
@@ -107,7 +110,10 @@ struct DeltaMmaCfg {
     static constexpr int RG = (P >= 11) ? 1 : (P == 7 ? QFS_DMMA_RG7 : (P == 5 ? QFS_DMMA_RG5 : P));  // rho1 values per class group
     static_assert(RG == 1 || RG == P, "class groups of unequal size are not supported (the column table is static)");
     static constexpr int NGROUP = (P + RG - 1) / RG;
-    static constexpr int NEC = NGROUP > 1 ? 3 : 1;               // coefficient-row buffers: in use, still read by a lagging warp, in flight
+    static constexpr int NBUF = (P >= 11) ? QFS_DMMA_NBUF11 : QFS_DMMA_NBUF;   // staging buffers (1: the copies of a phase overlap other CTAs' work only)
+    static constexpr int LAG = NBUF - 1;                             // phases an item warp may be behind the one that issues the prefetches
+    static constexpr int NEC = NGROUP > 1 ? 2 + LAG : 1;         // coefficient-row buffers: in use, (still read by a lagging warp,) in flight
+    static constexpr int XS = 2 + LAG;                           // slots of the class-0 terms: layers (s1-1,) s1, s1+1
     static constexpr int NCLS = RG * P * P;
     static constexpr int NCLS_PAD = (NCLS + 7) & ~7;
     static constexpr int NWI = (P >= 11) ? QFS_DMMA_NWI11 : (P == 7 ? QFS_DMMA_NWI7 : (P == 5 ? QFS_DMMA_NWI5 : 4));  // item warps
@@ -115,13 +121,12 @@ struct DeltaMmaCfg {
     static constexpr int NT = NTI + 32;                          // + the store warp
     static constexpr int SPLIT = (P >= 11) ? QFS_DMMA_SPLIT11 : 1;   // CTAs per quad of a large launch
     static constexpr int SPLIT_FEW = 16;                             // ... and when the launch has fewer quads than the GPU has SMs
-    static constexpr int NBUF = (P >= 11) ? 2 : QFS_DMMA_NBUF;       // staging buffers (1: the copies of a phase overlap other CTAs' work only)
     static constexpr int SBW = (P >= 13) ? QFS_DMMA_SBW13 : (P >= 11 ? QFS_DMMA_SBW11 : (P == 7 ? QFS_DMMA_SBW7 : (P == 5 ? QFS_DMMA_SBW5 : 2048)));  // words per staging buffer
     static constexpr int SBX = S::d + 5;                         // window side: 4 zero cells below (taps reach t2, t3 <= 4), u = 0..d
     static constexpr int PLANE = SBX * SBX;
     static constexpr int PLANE_PAD = (PLANE + 3) & ~3;           // words per plane (bulk copies move whole 16-byte units)
     static constexpr int PLANE_BYTES = 4 * PLANE_PAD;
-    static constexpr int RING = 6;                               // planes u1 = s1-4 .. s1 (a warp may lag a layer behind), s1+1 in flight
+    static constexpr int RING = 5 + LAG;                         // planes u1 = s1-3 .. s1 (one more if a warp may lag a layer behind), s1+1 in flight
     static constexpr int NPLANE = S::dh + 2;                     // planes of the global box: u1 = 0..dh and one of zeros
     static constexpr int TMAX_PAD = ((S::d + 1) * (S::d + 2) / 2 + 3) & ~3;   // points of the layer s1 = 0, in whole 16-byte units
     static QFS_HD constexpr int xoff(int s1)   // first word of layer s1 in the x region (every layer starts on 16 bytes)
@@ -137,8 +142,8 @@ struct DeltaMmaCfg {
     // shared memory (bytes)
     static constexpr int OFF_EC = 0;                                        // [NEC][4][NCLS_PAD][32]
     static constexpr int OFF_WIN = OFF_EC + NEC * 4 * NCLS_PAD * 32;        // uint32 [RING][PLANE_PAD]
-    static constexpr int OFF_X = OFF_WIN + RING * PLANE_BYTES;              // uint32 [3][TMAX_PAD]: the class-0 terms of layers s1-1, s1, s1+1
-    static constexpr int OFF_COL = OFF_X + 3 * TMAX_PAD * 4;                // int4 [NCLS_PAD]
+    static constexpr int OFF_X = OFF_WIN + RING * PLANE_BYTES;              // uint32 [XS][TMAX_PAD]: the class-0 terms of layers (s1-1,) s1, s1+1
+    static constexpr int OFF_COL = OFF_X + XS * TMAX_PAD * 4;               // int4 [NCLS_PAD]
     static constexpr int OFF_BAR = OFF_COL + NCLS_PAD * 16;                 // mbarriers: full[2], empty[2], window[RING], coefficient rows[3]
     static constexpr int OFF_STAGE = OFF_BAR + 128;
     static constexpr int SMEM = OFF_STAGE + NBUF * SBW * 4;
@@ -453,7 +458,7 @@ __device__ __forceinline__ void taps_to_surfaces(uint32_t w0, uint32_t w1, uint3
 
 template <int P>
 __global__ void __launch_bounds__(DeltaMmaCfg<P>::NT, DeltaMmaCfg<P>::MINB)
-k_delta_mma(const uint32_t* __restrict__ hbox_all, const uint8_t* __restrict__ A_all, const uint8_t* __restrict__ ecm_all,
+k_delta_mma(const uint32_t* __restrict__ hbox_all, const uint8_t* __restrict__ ecm_all,
             const DeltaPhase* __restrict__ phases, const DeltaPiece* __restrict__ pieces, const uint32_t* __restrict__ parts,
             uint8_t* __restrict__ delta_all, int count, int split)
 {
@@ -522,7 +527,7 @@ k_delta_mma(const uint32_t* __restrict__ hbox_all, const uint8_t* __restrict__ A
     // ---- item warps ---------------------------------------------------------------------------------------------------------------
     auto load_ec = [&](int idx, int rho1a, int nrho1) {   // one thread: the group's class rows of the live surfaces, load number idx
         const uint32_t bytes = (uint32_t)(nrho1 * P * P * 32);
-        const uint32_t bar = bEc + 8 * (idx % 3);
+        const uint32_t bar = bEc + 8 * (idx % C::NEC);
         mbar_expect_tx(bar, bytes * (uint32_t)nlive);
         for (int s = 0; s < nlive; ++s)
             bulk_g2s(aEc + (uint32_t)(((idx % C::NEC) * 4 + s) * C::NCLS_PAD * 32), ecm_all + (size_t)(4 * quad + s) * C::EC_STRIDE + (size_t)rho1a * P * P * 32,
@@ -535,10 +540,10 @@ k_delta_mma(const uint32_t* __restrict__ hbox_all, const uint8_t* __restrict__ A
         mbar_expect_tx(bWin + 8 * slot, C::PLANE_BYTES + xbytes);
         bulk_g2s(aWin + (uint32_t)(slot * C::PLANE_BYTES), hbox + (size_t)pl * C::PLANE_PAD, C::PLANE_BYTES, bWin + 8 * slot);
         if (with_x)
-            bulk_g2s(aX + (uint32_t)((u1 % 3) * C::TMAX_PAD * 4), hbox + (size_t)C::NPLANE * C::PLANE_PAD + C::xoff(u1), xbytes, bWin + 8 * slot);
+            bulk_g2s(aX + (uint32_t)((u1 % C::XS) * C::TMAX_PAD * 4), hbox + (size_t)C::NPLANE * C::PLANE_PAD + C::xoff(u1), xbytes, bWin + 8 * slot);
     };
     // No barrier among the item warps: a warp is never more than one phase behind another (two staging buffers), so a plane or
-    // a group of coefficient rows may be overwritten one block after its last use (RING = 6 planes, 3 row buffers), and every
+    // a group of coefficient rows may be overwritten one block after its last use (RING = 5 + LAG planes, 2 + LAG row buffers), and every
     // warp derives the same mbarrier parities from the phase list.
     int cur_s1 = -100, cur_grp = -1, ec_idx = -1, first_s1 = 0;
     int toffB[8];   // byte offsets (from a point's cell) of this thread's eight taps
@@ -573,7 +578,7 @@ k_delta_mma(const uint32_t* __restrict__ hbox_all, const uint8_t* __restrict__ A
                 mbar_wait(bWin + 8 * (s1 % C::RING), (uint32_t)(((s1 - first_s1 + 3) / C::RING) & 1));
             if (first || rho1a != cur_grp) {
                 ++ec_idx;
-                mbar_wait(bEc + 8 * (ec_idx % 3), (uint32_t)((ec_idx / 3) & 1));
+                mbar_wait(bEc + 8 * (ec_idx % C::NEC), (uint32_t)((ec_idx / C::NEC) & 1));
             }
             if (tid == 0) {
                 if (phd.flags & DPH_PF_PLANE) load_plane(s1 + 1, true);
@@ -634,7 +639,7 @@ k_delta_mma(const uint32_t* __restrict__ hbox_all, const uint8_t* __restrict__ A
         // ---- tiles (16 points x 8 classes), an equal share of the phase's nmt x ntile tiles per warp, in (point tile, class tile) order:
         //      the A fragments are gathered once per point tile of the share (at most twice per phase for most shares)
         const int T = nmt * ntile;
-        const uint32_t xrowB = aX + 4u * (uint32_t)((s1 % 3) * C::TMAX_PAD + s2a * (ns + 1) - (s2a * (s2a - 1)) / 2);   // the phase's first point
+        const uint32_t xrowB = aX + 4u * (uint32_t)((s1 % C::XS) * C::TMAX_PAD + s2a * (ns + 1) - (s2a * (s2a - 1)) / 2);   // the phase's first point
         int t = (wr * T) / C::NWI;
         const int t_hi = ((wr + 1) * T) / C::NWI;
         int mt = t / ntile, nt = t - mt * ntile;

@@ -420,7 +420,7 @@ int launch_delta(qfs_ctx* ctx, int count)
         const bool few = DM::SPLIT < DM::SPLIT_FEW && (int)quads * DM::MINB < ctx->sm_count;
         const int split = few ? DM::SPLIT_FEW : DM::SPLIT;
         k_delta_mma<P><<<quads * split, DM::NT, DM::SMEM, ctx->stream>>>(
-            ctx->hbox.as<uint32_t>(), ctx->A.as<uint8_t>(), ctx->ecm.as<uint8_t>(),
+            ctx->hbox.as<uint32_t>(), ctx->ecm.as<uint8_t>(),
             few ? ctx->dphases_few.as<DeltaPhase>() : ctx->dphases.as<DeltaPhase>(), ctx->dpieces.as<DeltaPiece>(),
             few ? ctx->dparts_few.as<uint32_t>() : ctx->dparts.as<uint32_t>(), ctx->delta.as<uint8_t>(), count, split);
         ctx->stats.kernel_launches++;

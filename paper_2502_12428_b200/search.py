@@ -186,7 +186,6 @@ def device_block(p: int, count: int, seed: int, worker: int, device: int = 0, bo
     back.  Returns (coeffs, codes, iters): coeffs is a torch CUDA tensor [count,35] (rows are fetched on demand), or a numpy array
     when the device reported a stream-shifting event (a Lemire rejection or a zero draw: about one block in 200 at 100 000
     rows) and the block was redrawn on the host -- either way the reference's samples, bit for bit."""
-    import torch
     from .engine import get_engine
     from .height import _check_engine_shape
     if not is_prime(p):
@@ -195,6 +194,14 @@ def device_block(p: int, count: int, seed: int, worker: int, device: int = 0, bo
     if method not in ("matrix", "naive"):
         raise DomainError(f"unknown method {method!r}, expected 'matrix' or 'naive'")
     eng = get_engine(p, device)
+    try:
+        import torch   # only to own the device buffer of the block
+    except ImportError:
+        host, clean = eng.sample(seed, worker, count)          # still drawn on the device, returned to the host
+        if not clean:
+            host = sample_block(p, count, seed, worker)
+        codes, iters = eng.heights(host, int(bound), matrix_free=(method == "naive"))
+        return host, codes, iters
     dev = torch.empty((count, NCOEFF), dtype=torch.uint8, device=f"cuda:{device}")
     _, clean = eng.sample(seed, worker, count, out=dev)
     if not clean:
