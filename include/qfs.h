@@ -163,6 +163,15 @@ int qfs_cubic_heights(int device, int p, const uint8_t *coeffs, size_t B, int bo
 int qfs_form_heights(int device, int p, int n, const uint8_t *coeffs, size_t B, int bound,
                      int8_t *heights, int8_t *iters);
 
+/* The reference's definitions executed literally on the device, for p = 3, 5, 7: g = f^(p-1) by dense multiplications
+ * (power_mod_p, polyring.py:253-272), Delta_1(g) = ((lift g)^p - sum of the p-th powers of its terms) / p mod p with the
+ * division checked (delta1, polyring.py:335-401), then g <- u(Delta g) until the Fedder coefficient survives (height_naive,
+ * height.py:97-116; split_u, polyring.py:295-313).  Shares no kernel and no identity with qfs_heights / qfs_heights_free: the
+ * on-device cross-check of both (a few ms per F_7 surface).  g_out [B][N] and delta_out [B][L] (dense, lex-ascending like the
+ * stage taps) may be NULL; every buffer may live on the host or on the device.  Context-free like qfs_cubic_heights. */
+int qfs_literal_heights(int device, int p, const uint8_t *coeffs, size_t B, int bound,
+                        int8_t *heights, int8_t *iters, uint8_t *g_out, uint8_t *delta_out);
+
 /* ---- export ---------------------------------------------------------------
  * Operator matrices of B quartics (given by their coefficient vectors) in the
  * reference's export layout: M16[B][N][N] row-major uint16 little-endian --

@@ -7,6 +7,7 @@ raise EngineUnavailableError.
 """
 from .cubic import Cubic, cubic_height_batch
 from .forms import Form, form_height_batch
+from .literal import literal_heights
 from .errors import DomainError, EngineUnavailableError, InternalInvariantError, ParseError, QfsplitError
 from .height import (INFINITE, HeightResult, SurfaceProblem, default_bound, height_batch, height_matrix,
                      height_naive, height_of_coeffs, is_prime)
@@ -34,7 +35,7 @@ __all__ = [
     "FixtureRow", "FixtureVerdict", "FoundSurface", "HeightHistogram", "SearchConfig", "found_surfaces_text",
     "histogram_text", "parse_fixtures", "run_search", "sample_block", "sample_surface", "spectrum_rows",
     "spectrum_search", "verify_fixtures", "fixtures_path",
-    "Cubic", "cubic_height_batch", "Form", "form_height_batch", "MtsMatrix", "build_mts", "build_mts_batch", "matrix_from_bytes", "matrix_from_text", "matrix_to_bytes",
+    "Cubic", "cubic_height_batch", "Form", "form_height_batch", "literal_heights", "MtsMatrix", "build_mts", "build_mts_batch", "matrix_from_bytes", "matrix_from_text", "matrix_to_bytes",
     "matrix_to_text", "target_degree",
     "DenseForm", "DenseVector", "delta1", "fedder_survives", "matvec", "power_mod_p", "to_dense",
 ]

@@ -19,6 +19,7 @@
 #include "qfs_delta_direct.cuh"
 #include "qfs_delta_mma.cuh"
 #include "qfs_form.cuh"
+#include "qfs_literal.cuh"
 #include "qfs_free.cuh"
 #include "qfs_matrix.cuh"
 #include "qfs_matrix_staged.cuh"
@@ -292,6 +293,12 @@ int build_tables(qfs_ctx* ctx)
         ctx->staged_multi = ((int)items.size() != S::ngroups);
         ctx->n_items = (int)items.size();
         ctx->staged_bufwords = SC::ZW + max_staged + SC::VWORDS;
+        if (getenv("QFS_VERBOSE")) {
+            long st = 0;
+            for (auto& t : tmp) st += t.staged;
+            fprintf(stderr, "qfs: p=%d builder panels %zu, staged entries per quad %ld (x4 bytes = %.2f x the 4 N^2 bytes written), largest %d\n", P,
+                    tmp.size(), st, (double)st / ((double)S::N * S::N), max_staged);
+        }
         // One staging buffer per CTA: with the arrive/sync split of k_matrix_staged a consumer must not be able to
         // run a quad ahead of the producer warp (more buffers would need one barrier per buffer).
         ctx->staged_smem = ctx->staged_nbuf * (size_t)ctx->staged_bufwords * 4;
@@ -1158,6 +1165,102 @@ int qfs_form_heights(int device, int p, int n, const uint8_t* coeffs, size_t B, 
     CUC(cudaMemcpy(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost));
     if (!h_dev) CUC(cudaMemcpy(heights, d_h, B, cudaMemcpyDeviceToHost));
     if (!i_dev) CUC(cudaMemcpy(iters, d_i, B, cudaMemcpyDeviceToHost));
+    CUC(cudaDeviceSynchronize());
+#undef CUC
+    cleanup();
+    if (h_err & QFS_ERRBIT_INPUT) return fail(ctx, QFS_EINVAL, "input violates a precondition: a coefficient >= p or the zero form");
+    if (h_err & QFS_ERRBIT_INVARIANT) return fail(ctx, QFS_EINVARIANT, "Witt-carry numerator not divisible by p");
+    return QFS_OK;
+}
+
+int qfs_literal_heights(int device, int p, const uint8_t* coeffs, size_t B, int bound, int8_t* heights, int8_t* iters, uint8_t* g_out,
+                        uint8_t* delta_out)
+{
+    qfs_ctx* ctx = nullptr;  // context-free: errors go where qfs_create's go, qfs_last_error(NULL)
+    if (p != 3 && p != 5 && p != 7) return fail(ctx, QFS_EINVAL, "the literal route runs for p = 3, 5, 7 (got p=%d)", p);
+    if (bound < 1 || bound > 127) return fail(ctx, QFS_EINVAL, "bound must be in 1..127, got %d", bound);
+    if (B == 0) return QFS_OK;
+    if (!coeffs || !heights || !iters) return fail(ctx, QFS_EINVAL, "NULL buffer");
+    if (B > 0x7fffffffULL) return fail(ctx, QFS_EINVAL, "batch too large");
+    const int d = 4 * (p - 1), D = p * d, W = D + 1;
+    const size_t boxsize = ((size_t)W * W * W + 15) & ~(size_t)15;
+    const size_t N = (size_t)qc3(d + 3), L = (size_t)qc3(D + 3);
+    DeviceGuard guard_(device);
+    const size_t chunk = std::max<size_t>(1, std::min<size_t>(std::min<size_t>(B, 8192), ((size_t)768 << 20) / (3 * boxsize)));
+    uint8_t *d_c = nullptr, *X = nullptr, *Y = nullptr, *Gb = nullptr, *dense = nullptr;
+    int8_t *d_h = nullptr, *d_i = nullptr;
+    LitTerm* terms = nullptr;
+    int *nterms = nullptr, *done = nullptr, *d_err = nullptr;
+    int rc = QFS_OK, h_err = 0;
+    auto cleanup = [&]() {
+        for (void* q : {(void*)d_c, (void*)X, (void*)Y, (void*)Gb, (void*)dense, (void*)d_h, (void*)d_i, (void*)terms, (void*)nterms, (void*)done, (void*)d_err})
+            if (q) cudaFree(q);
+    };
+#define CUC(call)                                                                                          \
+    do {                                                                                                   \
+        cudaError_t e_ = (call);                                                                           \
+        if (e_ != cudaSuccess) {                                                                           \
+            rc = fail(ctx, e_ == cudaErrorMemoryAllocation ? QFS_ENOMEM : QFS_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+            cleanup();                                                                                     \
+            return rc;                                                                                     \
+        }                                                                                                  \
+    } while (0)
+    CUC(cudaMalloc(&d_c, B * 35));
+    CUC(cudaMemcpy(d_c, coeffs, B * 35, cudaMemcpyDefault));
+    CUC(cudaMalloc(&d_h, B));
+    CUC(cudaMalloc(&d_i, B));
+    CUC(cudaMalloc(&X, chunk * boxsize));
+    CUC(cudaMalloc(&Y, chunk * boxsize));
+    CUC(cudaMalloc(&Gb, chunk * boxsize));
+    CUC(cudaMalloc(&terms, chunk * QFS_LIT_MAXTERMS * sizeof(LitTerm)));
+    CUC(cudaMalloc(&nterms, chunk * sizeof(int)));
+    CUC(cudaMalloc(&done, chunk * sizeof(int)));
+    CUC(cudaMalloc(&d_err, sizeof(int)));
+    CUC(cudaMemset(d_err, 0, sizeof(int)));
+    if (g_out || delta_out) CUC(cudaMalloc(&dense, chunk * (delta_out ? L : N)));
+    for (size_t first = 0; first < B; first += chunk) {
+        const unsigned cnt = (unsigned)std::min(chunk, B - first);
+        auto grid = [&](int deg) { return dim3((unsigned)((deg + 1) * (deg + 1)), cnt); };
+        uint8_t *cur = X, *other = Y;
+        // g = f^(p-1) mod p
+        k_lit_load<<<cnt, 32>>>(d_c, (int)first, p, W, boxsize, cur, d_err);
+        CUC(cudaMemsetAsync(nterms, 0, cnt * sizeof(int)));
+        k_lit_terms<<<grid(4), 32>>>(cur, 4, W, boxsize, terms, nterms);
+        for (int k = 2; k <= p - 1; ++k) {
+            k_lit_mul<<<grid(4 * k), QFS_LIT_NT>>>(cur, 4 * (k - 1), terms, nterms, 4, W, boxsize, other, p, nullptr);
+            std::swap(cur, other);
+        }
+        CUC(cudaMemcpyAsync(Gb, cur, cnt * boxsize, cudaMemcpyDeviceToDevice));
+        if (g_out) {
+            k_lit_dense<<<grid(d), 32>>>(Gb, d, W, boxsize, dense, N);
+            CUC(cudaMemcpy(g_out + first * N, dense, cnt * N, cudaMemcpyDefault));
+        }
+        k_lit_check<<<(cnt + 127) / 128, 128>>>(Gb, p, W, boxsize, 0, bound, (int)first, (int)cnt, d_h, d_i, done);
+        // Delta = ((lift g)^p - sum of the p-th powers of its terms) / p mod p; surfaces already decided are skipped unless Delta was asked for
+        const int* skip = delta_out ? nullptr : done;
+        CUC(cudaMemsetAsync(nterms, 0, cnt * sizeof(int)));
+        k_lit_terms<<<grid(d), 32>>>(Gb, d, W, boxsize, terms, nterms);
+        for (int k = 2; k <= p; ++k) {
+            k_lit_mul<<<grid(d * k), QFS_LIT_NT>>>(cur, d * (k - 1), terms, nterms, d, W, boxsize, other, p * p, skip);
+            std::swap(cur, other);
+        }
+        k_lit_carry<<<grid(D), 64>>>(cur, Gb, p, d, W, boxsize, d_err, skip);
+        if (delta_out) {
+            k_lit_dense<<<grid(D), 64>>>(cur, D, W, boxsize, dense, L);
+            CUC(cudaMemcpy(delta_out + first * L, dense, cnt * L, cudaMemcpyDefault));
+        }
+        // g <- u(Delta g)
+        uint8_t *ga = Gb, *gb = other;
+        for (int step = 1; step <= bound - 1; ++step) {
+            k_lit_step<<<grid(d), 32>>>(cur, ga, gb, done, p, d, W, boxsize);
+            std::swap(ga, gb);
+            k_lit_check<<<(cnt + 127) / 128, 128>>>(ga, p, W, boxsize, step, bound, (int)first, (int)cnt, d_h, d_i, done);
+        }
+        CUC(cudaGetLastError());
+    }
+    CUC(cudaMemcpy(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost));
+    CUC(cudaMemcpy(heights, d_h, B, cudaMemcpyDefault));
+    CUC(cudaMemcpy(iters, d_i, B, cudaMemcpyDefault));
     CUC(cudaDeviceSynchronize());
 #undef CUC
     cleanup();
