@@ -23,6 +23,10 @@ for p in primes:
     m = eng.export_matrix(c[:2])
     hf, itf = eng.heights(c, 10, matrix_free=True)
     assert np.array_equal(hs, hf) and np.array_equal(its, itf)
+    if p <= 7:   # the literal route (qfs_literal.cuh)
+        k = {3: 200, 5: 40, 7: 3}[p]
+        lh, li, lg, ld = q.literal_heights(p, c[:k], 10, want_g=True, want_delta=True)
+        assert np.array_equal(lh, hs[:k]) and np.array_equal(li, its[:k]) and np.array_equal(ld[:3], d)
     print(p, np.bincount(hs.astype(np.int64)).tolist(), d.shape, m.shape, flush=True)
 rng = np.random.default_rng(5)
 for p in (3, 5, 13):
