@@ -220,10 +220,19 @@ def algorithmic_bytes(p, iters_hard):
     }
 
 
+
+def host_threads():
+    """Host threads this process may use.  Not omp_get_max_threads(): torchrun exports OMP_NUM_THREADS=1 to its ranks, which
+    would turn the CPU arm of an N > 1 run into a single-thread baseline."""
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except (AttributeError, OSError):
+        return max(1, os.cpu_count() or 1)
+
 def cpu_baseline(p, coeffs, budget_s):
     """C oracle (port of the reference CPU algorithm) on all host threads, on a bounded prefix."""
     import oracle
-    threads = oracle.max_threads()
+    threads = host_threads()
     pilot = min(len(coeffs), 8 * threads)
     t0 = time.perf_counter()
     oracle.heights_batch(coeffs[:pilot], p, 10, threads)
@@ -246,7 +255,7 @@ def run_reference_arm(args):
     p = args.p
     coeffs = cached_block(p, min(args.batch, 20000), args.seed, 0)
     import oracle
-    threads = oracle.max_threads()
+    threads = host_threads()
     # size one step to ~ (120 s / (steps+warmup)) of CPU work
     pilot = 8 * threads
     t0 = time.perf_counter()
@@ -480,6 +489,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("QFS_BENCH_SHARE_GPU"):
+        local = 0   # test hook: every rank on cuda:0, to exercise the N > 1 path on a one-GPU box (not a measurement)
     dist = None
     if world > 1:
         import torch.distributed as dist_mod
