@@ -167,15 +167,24 @@ def height_batch(p: int, coeffs, bound: int = 10, devices=None, method: str = "m
 
     method: "matrix" (default; builds and streams the operator matrix like the reference's height_matrix) or
     "naive" (the polynomial iteration without the matrix, qfs_heights_free: the on-device counterpart of the
-    reference's height_naive cross-check; same heights and iteration counts).
+    reference's height_naive cross-check; same heights and iteration counts), or "literal" (p <= 7: the
+    reference's definitions executed literally on the device, csrc/qfs_literal.cuh -- the independent cross-check).
     out: optional pair of int8[B] numpy arrays to receive the results (e.g. pinned host memory).
     """
-    if method not in ("matrix", "naive"):
-        raise DomainError(f"unknown method {method!r}, expected 'matrix' or 'naive'")
+    if method not in ("matrix", "naive", "literal"):
+        raise DomainError(f"unknown method {method!r}, expected 'matrix', 'naive' or 'literal'")
     free = method == "naive"
     from .engine import get_engine
     c = _check_batch(p, coeffs, bound)
     B = c.shape[0]
+    if method == "literal":   # the reference's definitions executed literally (literal.py): the cross-check route, p <= 7, one device
+        from .literal import literal_heights
+        hs, its = literal_heights(p, c, int(bound), 0 if devices is None else int(list(devices)[0]))
+        if out is not None:
+            out[0][:] = hs
+            out[1][:] = its
+            return out[0], out[1]
+        return hs, its
     if out is not None:
         heights, iters = out
         for a in (heights, iters):

@@ -418,10 +418,11 @@ def verify_fixtures(text: str, n: int = 4, primes=None, jobs: int = 1, method: s
     """Recompute each fixture row's height on the GPU; verdicts in file order (search.py:219-229).
 
     Rows are grouped by prime and each group is one batched call.  `method` = "matrix" or "naive" as in the
-    reference ("naive" = the matrix-free polynomial iteration, csrc/qfs_free.cuh).
+    reference ("naive" = the matrix-free polynomial iteration, csrc/qfs_free.cuh); "literal" = the definitions executed
+    literally (csrc/qfs_literal.cuh, rows with p <= 7 only).
     `jobs` is ignored (one batched call replaces the reference's process pool).
     """
-    if method not in ("matrix", "naive"):
+    if method not in ("matrix", "naive", "literal"):
         raise DomainError(f"unknown method {method!r}")
     rows = parse_fixtures(text, n)
     if primes is not None:

@@ -58,6 +58,8 @@ def test_engine_agrees_with_the_literal_route(p, B, nd):
     c = rng.integers(0, p, size=(B, 35)).astype(np.uint8)
     c[(c == 0).all(axis=1), 0] = 1
     lh, li = literal_heights(p, c, 10)
+    hs, its = height_batch(p, c[:500], 10, method="literal")      # the same route through the batch entry
+    assert np.array_equal(hs, lh[:500]) and np.array_equal(its, li[:500])
     for method in ("matrix", "naive"):
         hs, its = height_batch(p, c, 10, method=method)
         bad = np.nonzero((hs != lh) | (its != li))[0]
@@ -87,3 +89,12 @@ def test_literal_bound_and_errors():
         literal_heights(5, bad, 10)
     with pytest.raises(DomainError):
         literal_heights(5, np.zeros((2, 35), dtype=np.uint8), 10)
+
+
+@pytest.mark.gpu
+def test_published_rows_through_the_literal_route():
+    """Every published row over F_3, F_5, F_7 (fixtures/k3_tables.txt, the paper's tables) by the literal computation."""
+    import paper_2502_12428_b200 as q
+    text = open(q.fixtures_path()).read()
+    verdicts = q.verify_fixtures(text, primes=[3, 5, 7], method="literal")
+    assert len(verdicts) == 22 and all(v.ok for v in verdicts), [(v.row.p, v.row.expected, v.got) for v in verdicts if not v.ok]
