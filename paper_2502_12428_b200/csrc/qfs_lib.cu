@@ -288,6 +288,22 @@ int build_tables(qfs_ctx* ctx)
         // Launch order = memory order of the rows (r1, r2 lexicographic, panels of a group adjacent): CTAs that
         // run at the same time write neighbouring rows, so their segments reach HBM together (measured: F_7
         // 38.1 -> 33.9 ms against a sort by decreasing work), and the grid ends with the short row groups.
+        {
+            // ... in T1 x T2 blocks of (r1, r2) where Delta does not fit L2 (p >= 11): a slab of Delta serves ~ (d+1)/p consecutive
+            // values of r1 (and of r2), and in plain lexicographic order a whole sweep over r2 lies between two of them, so the staged
+            // pieces are re-read from DRAM 3.5 x (F_11).  Measured (profiles/sweeps/r2_builder_experiments.txt): F_11 65.4 -> 62.4 ms
+            // per 20 000 surfaces with blocks of four r2, F_13 17.5 -> 17.0 ms with blocks of two r1; F_5 / F_7 are best unblocked.
+            int t1 = SC::ORDER_T1, t2 = SC::ORDER_T2;
+            if (const char* e = getenv("QFS_PANEL_ORDER")) {
+                if (sscanf(e, "%d,%d", &t1, &t2) != 2 || t1 < 1 || t2 < 1) { t1 = SC::ORDER_T1; t2 = SC::ORDER_T2; }
+            }
+            if (t1 > 1 || t2 > 1)
+                std::stable_sort(tmp.begin(), tmp.end(), [&](const Tmp& a, const Tmp& b) {
+                    const int ka[4] = {a.it.r1 / t1, a.it.r2 / t2, a.it.r1 % t1, a.it.r2 % t2};
+                    const int kb[4] = {b.it.r1 / t1, b.it.r2 / t2, b.it.r1 % t1, b.it.r2 % t2};
+                    return std::lexicographical_compare(ka, ka + 4, kb, kb + 4);
+                });
+        }
         std::vector<PanelItem> items(tmp.size());
         for (size_t i = 0; i < tmp.size(); ++i) items[i] = tmp[i].it;
         ctx->staged_multi = ((int)items.size() != S::ngroups);

@@ -95,6 +95,9 @@ struct StagedCfg {
     static constexpr int MAXC = S::d + 2;                    // pieces per panel
     static constexpr int BUDGET = (P >= 13) ? QFS_BUDGET13 : (P >= 11 ? QFS_BUDGET11 : (P == 7 ? QFS_BUDGET7 : (P == 5 ? QFS_BUDGET5 : 12800)));  // default staged entries (x4 bytes) per panel
     static constexpr size_t MSTRIDE = (size_t)S::N * S::pitch;
+    // launch order of the row groups: blocks of ORDER_T1 values of r1 x ORDER_T2 values of r2 (1 x 1: lexicographic); see build_tables
+    static constexpr int ORDER_T1 = (P == 13) ? 2 : (P == 11 ? S::d + 1 : 1);
+    static constexpr int ORDER_T2 = (P == 11) ? 4 : 1;
     static constexpr int VSEG = MAXG * 4 * V + 16;           // bytes of one surface's slice of v0 staged per buffer (16-byte aligned window)
     static constexpr int VWORDS = 4 * VSEG / 4;              // 32-bit words of the v0 area at the end of a buffer
     static_assert(WORDS % V == 0 && TEAM % 32 == 0 || P == 3, "teams are whole warps");
