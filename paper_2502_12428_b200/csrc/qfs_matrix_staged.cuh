@@ -90,7 +90,10 @@ struct StagedCfg {
     // glo % LINEG threads in front of the panel repeat its first word group.
     static constexpr int LINEG = (QFS_PITCH_ALIGN % 128 == 0) ? 128 / (4 * V) : 1;
     static constexpr int MAXROWS = S::d + 1;
-    static constexpr int SLICE = (P >= 11) ? QFS_SLICE11 : (P >= 7 ? QFS_SLICE7 : QFS_SLICE5);        // quads per CTA
+#ifndef QFS_SLICE13
+#define QFS_SLICE13 QFS_SLICE11
+#endif
+    static constexpr int SLICE = (P >= 13) ? QFS_SLICE13 : (P >= 11 ? QFS_SLICE11 : (P >= 7 ? QFS_SLICE7 : QFS_SLICE5));        // quads per CTA
     static constexpr int ZW = (P * S::d + 4 + 3) & ~3;       // zero region (entries) read by columns that never match
     static constexpr int MAXC = S::d + 2;                    // pieces per panel
     static constexpr int BUDGET = (P >= 13) ? QFS_BUDGET13 : (P >= 11 ? QFS_BUDGET11 : (P == 7 ? QFS_BUDGET7 : (P == 5 ? QFS_BUDGET5 : 12800)));  // default staged entries (x4 bytes) per panel
