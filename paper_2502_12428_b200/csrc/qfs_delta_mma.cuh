@@ -110,6 +110,7 @@ struct DeltaMmaCfg {
     static constexpr int RG = (P >= 11) ? 1 : (P == 7 ? QFS_DMMA_RG7 : (P == 5 ? QFS_DMMA_RG5 : P));  // rho1 values per class group
     static_assert(RG == 1 || RG == P, "class groups of unequal size are not supported (the column table is static)");
     static constexpr int NGROUP = (P + RG - 1) / RG;
+    static constexpr bool STORE_GUARDS = (RG == 1);              // the store warp writes the guard zeros (see k_delta_mma)
     static constexpr int NBUF = (P >= 11) ? QFS_DMMA_NBUF11 : QFS_DMMA_NBUF;   // staging buffers (1: the copies of a phase overlap other CTAs' work only)
     static constexpr int LAG = NBUF - 1;                             // phases an item warp may be behind the one that issues the prefetches
     static constexpr int NEC = NGROUP > 1 ? 2 + LAG : 1;         // coefficient-row buffers: in use, (still read by a lagging warp,) in flight
@@ -502,22 +503,62 @@ k_delta_mma(const uint32_t* __restrict__ hbox_all, const uint8_t* __restrict__ e
     fence_proxy_async();
     __syncthreads();
 
+    // GUARD ZEROS of a phase, a run per lane: the gap in front of the run and, after the last run of a piece, the rest of the piece.
+    // With the entries these are all the words of the phase (tools/check_delta_plan.cpp), so nothing ever clears a buffer.
+    // Who writes them (C::STORE_GUARDS): with one rho1 per phase (p >= 7) the store warp, right after the copies of phase li have read
+    // the buffer and while the item warps are already writing the entries of phase li + NBUF (disjoint words) -- F_7 -4 %, F_11 -4 %,
+    // F_13 -9 %; with all rho1 in a phase (p <= 5: ~200 runs per phase) one warp would be the critical path (F_5 +7 %), so there
+    // every item warp zeroes its share of the runs before its tiles.
+    auto guards = [&](const DeltaPhase& ph, const DeltaPiece& pcl, int b, int share, int nshare) {
+        const int nrho1 = ph.nrho1, s2a = ph.s2a;
+        const int n0 = S::D - P * ph.s1 - ph.rho1a;
+        const int per = P * (ph.s2b - s2a);
+        const int nruns = nrho1 * per;   // (slab, run) pairs of the phase
+        const uint32_t stageB = aStage + 4u * (uint32_t)(b * C::SBW);
+        const int g_hi = ((share + 1) * nruns) / nshare;
+        for (int g0 = (share * nruns) / nshare; g0 < g_hi; g0 += 32) {   // uniform trip count: the shuffles need every lane
+            const int gi = g0 + lane;
+            const int k = min(gi / per, nrho1 - 1), j = gi - k * per;
+            const int I2 = P * s2a + j, nk = n0 - k;
+            const int pcc = __shfl_sync(0xffffffffu, pcl.cconst, k), ppo = __shfl_sync(0xffffffffu, (int)pcl.po, k),
+                      pnw = __shfl_sync(0xffffffffu, (int)pcl.nw, k);
+            if (gi >= g_hi) continue;
+            if (I2 <= nk && pnw > 0) {
+                const int rs = delta_run_start<P>(nk, I2, pcc, ppo);
+                const uint32_t pieceB = stageB + 4u * (uint32_t)ppo;
+                for (int w = (j == 0 ? 0 : rs - S::G); w < rs; ++w) sts32(pieceB + 4u * (uint32_t)w, 0u);
+                if (I2 == min(P * (int)ph.s2b - 1, nk))
+                    for (int w = rs + (nk - I2 + 1); w < pnw; ++w) sts32(pieceB + 4u * (uint32_t)w, 0u);
+            }
+        }
+    };
     // ---- store warp: a phase's pieces leave with bulk copies as soon as every item warp has delivered ----------------------------
     if (warp == C::NWI) {
         // lane k owns piece k of a phase; the descriptors of the next phase are fetched before the wait (no global latency in the chain)
         DeltaPhase phd = phases[pa];
         DeltaPiece pc = pieces[phd.piece0 + min(lane, (int)phd.nrho1 - 1)];
+        if (C::STORE_GUARDS) {
+            guards(phd, pc, 0, 0, 1);
+            if (C::NBUF > 1 && nph > 1) {
+                const DeltaPhase p1 = phases[pa + 1];
+                guards(p1, pieces[p1.piece0 + min(lane, (int)p1.nrho1 - 1)], 1, 0, 1);
+            }
+        }
         for (int li = 0; li < nph; ++li) {
             const int b = li % C::NBUF;
             const DeltaPhase nphd = phases[pa + min(li + 1, nph - 1)];
             const DeltaPiece npc = pieces[nphd.piece0 + min(lane, (int)nphd.nrho1 - 1)];
+            const DeltaPhase gph = phases[pa + min(li + C::NBUF, nph - 1)];          // the phase that gets this buffer next
+            const DeltaPiece gpc = pieces[gph.piece0 + min(lane, (int)gph.nrho1 - 1)];
             if (lane == 0) mbar_wait_backoff(bFull + 8 * b, (uint32_t)((li / C::NBUF) & 1));
+            fence_proxy_async();   // this warp's guard zeros, too, are visible to the copy engine
             __syncwarp();
             if (lane < phd.nrho1 && pc.nw) bulk_s2g(gq + 4 * (size_t)pc.ga, aStage + 4u * (uint32_t)(b * C::SBW + (int)pc.po), pc.nw * 4u);
             bulk_commit();
             bulk_wait_read0();
             __syncwarp();
             if (lane == 0) mbar_arrive(bEmpty + 8 * b);
+            if (C::STORE_GUARDS && li + C::NBUF < nph) guards(gph, gpc, b, 0, 1);
             phd = nphd;
             pc = npc;
         }
@@ -613,28 +654,7 @@ k_delta_mma(const uint32_t* __restrict__ hbox_all, const uint8_t* __restrict__ e
         const int ntile = (ncls + 7) >> 3;
         const int wr = (warp + li) % C::NWI;   // rotate the shares: the remainders do not always hit the same warps
 
-        // ---- guard zeros, a run per lane: the gap in front of the run and, after the last run of a piece, the rest of the piece.
-        //      With the entries these are all the words of the phase (tools/check_delta_plan.cpp), so nothing clears the buffer.
-        {
-            const int per = P * (phd.s2b - s2a);
-            const int nruns = nrho1 * per;   // (slab, run) pairs of the phase
-            const int g_hi = ((wr + 1) * nruns) / C::NWI;
-            for (int g0 = (wr * nruns) / C::NWI; g0 < g_hi; g0 += 32) {   // uniform trip count: the shuffles need every lane
-                const int gi = g0 + lane;
-                const int k = min(gi / per, nrho1 - 1), j = gi - k * per;
-                const int I2 = P * s2a + j, nk = n0 - k;
-                const int pcc = __shfl_sync(0xffffffffu, mypc.cconst, k), ppo = __shfl_sync(0xffffffffu, (int)mypc.po, k),
-                          pnw = __shfl_sync(0xffffffffu, (int)mypc.nw, k);
-                if (gi >= g_hi) continue;
-                if (I2 <= nk && pnw > 0) {
-                    const int rs = delta_run_start<P>(nk, I2, pcc, ppo);
-                    const uint32_t pieceB = stageB + 4u * (uint32_t)ppo;
-                    for (int w = (j == 0 ? 0 : rs - S::G); w < rs; ++w) sts32(pieceB + 4u * (uint32_t)w, 0u);
-                    if (I2 == min(P * (int)phd.s2b - 1, nk))
-                        for (int w = rs + (nk - I2 + 1); w < pnw; ++w) sts32(pieceB + 4u * (uint32_t)w, 0u);
-                }
-            }
-        }
+        if (!C::STORE_GUARDS) guards(phd, mypc, b, wr, C::NWI);
 
         // ---- tiles (16 points x 8 classes), an equal share of the phase's nmt x ntile tiles per warp, in (point tile, class tile) order:
         //      the A fragments are gathered once per point tile of the share (at most twice per phase for most shares)
