@@ -74,7 +74,7 @@ struct DeltaPiece {
 #define QFS_DMMA_SBW5 6144
 #endif
 #ifndef QFS_DMMA_SBW7
-#define QFS_DMMA_SBW7 6144
+#define QFS_DMMA_SBW7 5600   // 57.3 KB per CTA: four CTAs per SM (6144 words are 48 bytes too many for that: 9.4 -> 8.3 ms)
 #endif
 #ifndef QFS_DMMA_SBW11
 #define QFS_DMMA_SBW11 12288
@@ -110,7 +110,10 @@ struct DeltaMmaCfg {
     static constexpr int RG = (P >= 11) ? 1 : (P == 7 ? QFS_DMMA_RG7 : (P == 5 ? QFS_DMMA_RG5 : P));  // rho1 values per class group
     static_assert(RG == 1 || RG == P, "class groups of unequal size are not supported (the column table is static)");
     static constexpr int NGROUP = (P + RG - 1) / RG;
-    static constexpr bool STORE_GUARDS = (RG == 1);              // the store warp writes the guard zeros (see k_delta_mma)
+#ifndef QFS_DMMA_STORE_GUARDS
+#define QFS_DMMA_STORE_GUARDS 1
+#endif
+    static constexpr bool STORE_GUARDS = (RG == 1) && QFS_DMMA_STORE_GUARDS;   // the store warp writes the guard zeros (see k_delta_mma)
     static constexpr int NBUF = (P >= 11) ? QFS_DMMA_NBUF11 : QFS_DMMA_NBUF;   // staging buffers (1: the copies of a phase overlap other CTAs' work only)
     static constexpr int LAG = NBUF - 1;                             // phases an item warp may be behind the one that issues the prefetches
     static constexpr int NEC = NGROUP > 1 ? 2 + LAG : 1;         // coefficient-row buffers: in use, (still read by a lagging warp,) in flight
@@ -150,6 +153,8 @@ struct DeltaMmaCfg {
     static constexpr int SMEM = OFF_STAGE + NBUF * SBW * 4;
     static constexpr int MINB_S = (228 * 1024) / (SMEM + 1024);   // CTAs per SM that shared memory allows
     static constexpr int MINB = MINB_S < 1 ? 1 : (MINB_S > QFS_DMMA_MAXB ? QFS_DMMA_MAXB : MINB_S);   // register budget: that many CTAs of NT threads
+    static_assert(P != 7 || MINB == 4, "k_delta_mma<7> is tuned for four CTAs per SM: shared memory grew past 57 344 bytes");
+    static_assert(P != 5 || MINB == 4, "k_delta_mma<5> is tuned for four CTAs per SM");
     static_assert(MAGIC * P - 65536u < 65536u / (35u * (P - 1) * (P - 1) + P), "magic quotient not exact");
 };
 
