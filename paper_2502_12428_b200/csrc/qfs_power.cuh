@@ -53,6 +53,9 @@ struct PowerCfg {
     static constexpr int FED_BUF = qround16(qc3(4 * J0 + 3));
     static constexpr int RB_DEG = 4 * P;                // row-base tables up to this degree
     static constexpr int FULL_NT = 256;
+    // CTAs per SM k_power_full is compiled for: shared memory allows 7 (p = 5), 5 (p = 7), 1 (p >= 11); at p <= 5 the 35
+    // multiplier coefficients otherwise sit in 55 registers and leave room for four CTAs only (F_5: 0.555 -> 0.49 ms)
+    static constexpr int FULL_MINB = (P <= 5) ? 8 : (P == 7 ? 5 : 1);
     static constexpr int FULL_BUF = S::NE_pad;
     // row-base tables rb_d for d = 4, 8, ..., RB_DEG; table d starts at rb_offset(d)
     static QFS_HD constexpr int rb_offset(int d) { return qrb_offset(d); }
@@ -238,7 +241,7 @@ k_fedder(const uint8_t* __restrict__ coeffs, int count, const uint32_t* __restri
 
 // ---------------------------------------------------------------------------------------------
 template <int P>
-__global__ void __launch_bounds__(PowerCfg<P>::FULL_NT)
+__global__ void __launch_bounds__(PowerCfg<P>::FULL_NT, PowerCfg<P>::FULL_MINB)
 k_power_full(const uint8_t* __restrict__ coeffs, const uint32_t* __restrict__ list, int count,
              const uint32_t* __restrict__ unrank, uint8_t* __restrict__ fedder_out,
              uint8_t* __restrict__ g_out, uint8_t* __restrict__ h_out,
