@@ -202,6 +202,11 @@ int qfs_sample_quartics(qfs_ctx *ctx, const uint64_t state_inc[4], size_t count,
  * workspaces between calls to prove it. */
 int qfs_debug_fill_workspaces(qfs_ctx *ctx, int byte);
 
+/* Resident CTAs per SM of the stage kernels as built and configured on this device (cudaOccupancyMaxActiveBlocksPerMultiprocessor):
+ * [0] k_power_full, [1] k_delta_mma, [2] k_matrix_staged (with the fused first step), [3] k_chain.  The kernels are tuned for
+ * specific counts; tests/test_gpu_api.py pins them so that a change that costs a CTA per SM is noticed. */
+int qfs_debug_occupancy(const qfs_ctx *ctx, int ctas_per_sm[4]);
+
 #ifdef __cplusplus
 }
 #endif

@@ -22,7 +22,7 @@ EXPORTS = (
     "qfs_set_workspace_limit", "qfs_set_chunk", "qfs_heights", "qfs_heights_free", "qfs_get_stats",
     "qfs_stage_power", "qfs_stage_delta", "qfs_stage_matrix", "qfs_stage_matvec_chain",
     "qfs_export_matrix", "qfs_debug_fill_workspaces", "qfs_cubic_heights", "qfs_sample_quartics", "qfs_form_heights",
-    "qfs_literal_heights",
+    "qfs_literal_heights", "qfs_debug_occupancy",
 )
 
 
@@ -91,6 +91,7 @@ def load():
     lib.qfs_stage_matvec_chain.argtypes = [vp, u8p, u8p, sz, ctypes.c_int, u8p, i8p, i8p]
     lib.qfs_export_matrix.argtypes = [vp, u8p, sz, vp]
     lib.qfs_debug_fill_workspaces.argtypes = [vp, ctypes.c_int]
+    lib.qfs_debug_occupancy.argtypes = [vp, ctypes.POINTER(ctypes.c_int)]
     lib.qfs_cubic_heights.argtypes = [ctypes.c_int, ctypes.c_int, u8p, sz, ctypes.c_int, i8p, i8p]
     lib.qfs_form_heights.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, u8p, sz, ctypes.c_int, i8p, i8p]
     lib.qfs_literal_heights.argtypes = [ctypes.c_int, ctypes.c_int, u8p, sz, ctypes.c_int, i8p, i8p, u8p, u8p]

@@ -101,6 +101,7 @@ struct qfs_ctx {
     size_t staged_smem = 0;
     int staged_bufwords = 0;
     int staged_nbuf = 1;
+    int occ[4] = {0, 0, 0, 0};   // resident CTAs per SM: k_power_full, k_delta_mma, k_matrix_staged (fused), k_chain
     int staged_multi = 0;
     int delta_direct = 0;                           // QFS_DELTA_DIRECT: use k_delta_direct for every prime (cross-check)
     int delta_version = 2;                          // QFS_DELTA_V: 2 = tensor-core kernel (k_delta_mma), 1 = DP4A slab kernel (k_delta)
@@ -371,6 +372,17 @@ int build_tables(qfs_ctx* ctx)
     }
     if (const char* e = getenv("QFS_CHAIN_GRID")) ctx->chain_grid_mode = atoi(e);
     CU(cudaFuncSetAttribute(k_chain<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, ChainCfg<P>::SMEM));
+    // resident CTAs per SM of the four stage kernels as built and configured (qfs_debug_occupancy): a few bytes of shared memory
+    // or a few registers too many silently cost a CTA per SM (k_delta_mma<7> ran on three instead of four for half a round)
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->occ[0], k_power_full<P>, PowerCfg<P>::FULL_NT, PowerCfg<P>::FULL_SMEM));
+    ctx->occ[1] = 0;
+    if constexpr (P >= 3 && DeltaMmaCfg<P>::SMEM <= 227 * 1024)
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->occ[1], k_delta_mma<P>, DeltaMmaCfg<P>::NT, DeltaMmaCfg<P>::SMEM));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->occ[2], k_matrix_staged<P, true>, StagedCfg<P>::NTL, ctx->staged_smem));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->occ[3], k_chain<P>, ChainCfg<P>::NT, ChainCfg<P>::SMEM));
+    if (getenv("QFS_VERBOSE"))
+        fprintf(stderr, "qfs: p=%d CTAs per SM: k_power_full %d, k_delta_mma %d, k_matrix_staged %d, k_chain %d\n", P, ctx->occ[0], ctx->occ[1],
+                ctx->occ[2], ctx->occ[3]);
     return QFS_OK;
 }
 
@@ -1282,6 +1294,13 @@ int qfs_literal_heights(int device, int p, const uint8_t* coeffs, size_t B, int 
     cleanup();
     if (h_err & QFS_ERRBIT_INPUT) return fail(ctx, QFS_EINVAL, "input violates a precondition: a coefficient >= p or the zero form");
     if (h_err & QFS_ERRBIT_INVARIANT) return fail(ctx, QFS_EINVARIANT, "Witt-carry numerator not divisible by p");
+    return QFS_OK;
+}
+
+int qfs_debug_occupancy(const qfs_ctx* ctx, int ctas_per_sm[4])
+{
+    if (!ctx || !ctas_per_sm) return QFS_EINVAL;
+    for (int i = 0; i < 4; ++i) ctas_per_sm[i] = ctx->occ[i];
     return QFS_OK;
 }
 

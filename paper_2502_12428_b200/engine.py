@@ -81,6 +81,12 @@ class Engine:
     def set_chunk(self, n):
         self._call(self.lib.qfs_set_chunk, int(n))
 
+    def occupancy(self):
+        """Resident CTAs per SM of k_power_full, k_delta_mma, k_matrix_staged, k_chain as built (qfs_debug_occupancy)."""
+        out = (ctypes.c_int * 4)()
+        self._check(self.lib.qfs_debug_occupancy(self._h, out))
+        return dict(zip(("k_power_full", "k_delta_mma", "k_matrix_staged", "k_chain"), (int(x) for x in out)))
+
     def stats(self):
         st = _native.QfsStats()
         self._check(self.lib.qfs_get_stats(self._h, ctypes.byref(st)))

@@ -398,3 +398,14 @@ def test_spectrum_search_on_the_gpu_and_its_witnesses():
     # the matrix-free mode finds the same witnesses (same blocks, same heights)
     wit2, hist2, blocks2 = q.spectrum_search(5, block=100000, rng_seed=0, max_blocks=400, method="naive")
     assert blocks2 == blocks and {h: w[:2] for h, w in wit2.items()} == {h: w[:2] for h, w in wit.items()}
+
+
+@pytest.mark.parametrize("p,want", [(5, (8, 4, 7, 2)), (7, (5, 4, 6, 2)), (11, (1, 1, 3, 1))])
+def test_stage_kernels_keep_their_resident_cta_counts(p, want):
+    """The stage kernels are tuned for specific CTA counts per SM; a few bytes of shared memory or a few
+    registers too many cost one silently (k_delta_mma<7> ran on three CTAs instead of four for half of round 2)."""
+    from paper_2502_12428_b200.engine import get_engine
+    occ = get_engine(p, 0).occupancy()
+    got = (occ["k_power_full"], occ["k_delta_mma"], occ["k_matrix_staged"], occ["k_chain"])
+    for name, g, w in zip(("k_power_full", "k_delta_mma", "k_matrix_staged", "k_chain"), got, want):
+        assert w is None or g >= w, f"{name}<{p}>: {g} resident CTAs per SM, tuned for {w}"
