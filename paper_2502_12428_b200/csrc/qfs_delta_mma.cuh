@@ -124,7 +124,11 @@ struct DeltaMmaCfg {
     static constexpr int NTI = 32 * NWI;
     static constexpr int NT = NTI + 32;                          // + the store warp
     static constexpr int SPLIT = (P >= 11) ? QFS_DMMA_SPLIT11 : 1;   // CTAs per quad of a large launch
-    static constexpr int SPLIT_FEW = 16;                             // ... and when the launch has fewer quads than the GPU has SMs
+    // ... of a launch with fewer quads than CTA slots (SPLIT_MID), and of one with at most four quads (SPLIT_FEW: single surfaces).
+    // Measured: one F_7 surface 0.34 -> 0.25 ms and one F_11 surface 1.16 -> 0.79 ms per call with 256 parts instead of 16; 40 F_13
+    // quads 4.96 -> 4.52 ms with 64; 94 F_11 quads are best at 16 ... 64 and lose 11 % at 256.
+    static constexpr int SPLIT_MID = 64;
+    static constexpr int SPLIT_FEW = 256;
     static constexpr int SBW = (P >= 13) ? QFS_DMMA_SBW13 : (P >= 11 ? QFS_DMMA_SBW11 : (P == 7 ? QFS_DMMA_SBW7 : (P == 5 ? QFS_DMMA_SBW5 : 2048)));  // words per staging buffer
     static constexpr int SBX = S::d + 5;                         // window side: 4 zero cells below (taps reach t2, t3 <= 4), u = 0..d
     static constexpr int PLANE = SBX * SBX;

@@ -106,7 +106,8 @@ struct qfs_ctx {
     int delta_direct = 0;                           // QFS_DELTA_DIRECT: use k_delta_direct for every prime (cross-check)
     int delta_version = 2;                          // QFS_DELTA_V: 2 = tensor-core kernel (k_delta_mma), 1 = DP4A slab kernel (k_delta)
     DevBuf ecm, hbox, dphases, dpieces, dparts;     // k_delta_mma: class-major coefficient tables and interleaved h boxes (chunk-sized), phase plan
-    DevBuf dphases_few, dparts_few;                 // the same plan cut into SPLIT_FEW parts per quad (launches of a few quads)
+    DevBuf dphases_few, dparts_few;                 // the same plan cut into SPLIT_FEW parts per quad (launches of at most four quads)
+    DevBuf dphases_mid, dparts_mid;                 // ... and into SPLIT_MID parts (fewer quads than CTA slots)
     int matrix_version = 6;                         // 6 = shared-memory staged builder, 4 = direct gather (QFS_MATRIX_V)
     int* h_flags = nullptr;                         // pinned mirror of flags
 };
@@ -349,6 +350,12 @@ int build_tables(qfs_ctx* ctx)
         CU(ctx->dparts_few.reserve(few.parts.size() * sizeof(uint32_t)));
         CU(cudaMemcpy(ctx->dphases_few.ptr, few.phases.data(), few.phases.size() * sizeof(DeltaPhase), cudaMemcpyHostToDevice));
         CU(cudaMemcpy(ctx->dparts_few.ptr, few.parts.data(), few.parts.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+        DeltaPlan mid;
+        if (!delta_plan<P>(mid, DeltaMmaCfg<P>::SPLIT_MID)) return fail(ctx, QFS_EINVAL, "internal: Witt-carry plan does not fit its buffers");
+        CU(ctx->dphases_mid.reserve(mid.phases.size() * sizeof(DeltaPhase)));
+        CU(ctx->dparts_mid.reserve(mid.parts.size() * sizeof(uint32_t)));
+        CU(cudaMemcpy(ctx->dphases_mid.ptr, mid.phases.data(), mid.phases.size() * sizeof(DeltaPhase), cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(ctx->dparts_mid.ptr, mid.parts.data(), mid.parts.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
         CU(cudaFuncSetAttribute(k_delta_mma<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, DeltaMmaCfg<P>::SMEM));
         CU(cudaFuncSetAttribute(k_delta_box<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * Shape<P>::Nh_pad));
     }
@@ -452,12 +459,13 @@ int launch_delta(qfs_ctx* ctx, int count)
         ctx->stats.kernel_launches += 2;
         CU(cudaGetLastError());
         // few quads (single surfaces, small batches): more CTAs per quad, so that the launch still covers the SMs
-        const bool few = DM::SPLIT < DM::SPLIT_FEW && (int)quads * DM::MINB < ctx->sm_count;
-        const int split = few ? DM::SPLIT_FEW : DM::SPLIT;
-        k_delta_mma<P><<<quads * split, DM::NT, DM::SMEM, ctx->stream>>>(
-            ctx->hbox.as<uint32_t>(), ctx->ecm.as<uint8_t>(),
-            few ? ctx->dphases_few.as<DeltaPhase>() : ctx->dphases.as<DeltaPhase>(), ctx->dpieces.as<DeltaPiece>(),
-            few ? ctx->dparts_few.as<uint32_t>() : ctx->dparts.as<uint32_t>(), ctx->delta.as<uint8_t>(), count, split);
+        const int level = ((int)quads <= 4 && DM::SPLIT < DM::SPLIT_FEW) ? 2 : (((int)quads * DM::MINB < ctx->sm_count && DM::SPLIT < DM::SPLIT_MID) ? 1 : 0);
+        const int split = level == 2 ? DM::SPLIT_FEW : (level == 1 ? DM::SPLIT_MID : DM::SPLIT);
+        const DevBuf& ph = level == 2 ? ctx->dphases_few : (level == 1 ? ctx->dphases_mid : ctx->dphases);
+        const DevBuf& pt = level == 2 ? ctx->dparts_few : (level == 1 ? ctx->dparts_mid : ctx->dparts);
+        k_delta_mma<P><<<quads * split, DM::NT, DM::SMEM, ctx->stream>>>(ctx->hbox.as<uint32_t>(), ctx->ecm.as<uint8_t>(), ph.as<DeltaPhase>(),
+                                                                         ctx->dpieces.as<DeltaPiece>(), pt.as<uint32_t>(), ctx->delta.as<uint8_t>(),
+                                                                         count, split);
         ctx->stats.kernel_launches++;
         CU(cudaGetLastError());
         return QFS_OK;
@@ -954,7 +962,7 @@ void qfs_destroy(qfs_ctx* ctx)
     DeviceGuard guard_(ctx->device);
     DevBuf* bufs[] = {&ctx->flags, &ctx->colinfo, &ctx->groups, &ctx->runs, &ctx->unrank, &ctx->coeffs, &ctx->heights, &ctx->iters, &ctx->list,
                       &ctx->g, &ctx->h, &ctx->A, &ctx->E, &ctx->delta, &ctx->M, &ctx->v1, &ctx->tapA, &ctx->tapB, &ctx->items, &ctx->vacc, &ctx->chain_scratch,
-                      &ctx->ecm, &ctx->hbox, &ctx->dphases_few, &ctx->dparts_few, &ctx->dphases, &ctx->dpieces, &ctx->dparts};
+                      &ctx->ecm, &ctx->hbox, &ctx->dphases_few, &ctx->dparts_few, &ctx->dphases_mid, &ctx->dparts_mid, &ctx->dphases, &ctx->dpieces, &ctx->dparts};
     for (DevBuf* b : bufs) b->release();
     for (auto& e : ctx->ev) if (e) cudaEventDestroy(e);
     for (auto& e : ctx->ev_total) if (e) cudaEventDestroy(e);

@@ -14,4 +14,4 @@ def test_delta_plan_covers_delta_exactly_once(tmp_path):
     out = subprocess.run([exe], capture_output=True, text=True)
     sys.stdout.write(out.stdout)
     assert out.returncode == 0, out.stdout + out.stderr
-    assert out.stdout.count(": ok") == 7
+    assert out.stdout.count(": ok") == 10

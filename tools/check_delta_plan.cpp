@@ -119,7 +119,10 @@ int main()
     e += check<7>();
     e += check<11>();
     e += check<13>();
-    e += check<5>(DeltaMmaCfg<5>::SPLIT_FEW);   // the plan of launches with few quads
+    e += check<5>(DeltaMmaCfg<5>::SPLIT_FEW);   // the plans of launches with few quads
+    e += check<7>(DeltaMmaCfg<7>::SPLIT_MID);
     e += check<7>(DeltaMmaCfg<7>::SPLIT_FEW);
+    e += check<11>(DeltaMmaCfg<11>::SPLIT_FEW);
+    e += check<3>(DeltaMmaCfg<3>::SPLIT_FEW);
     return e ? 1 : 0;
 }
