@@ -53,10 +53,10 @@ struct StagedCfg {
 #define QFS_NT5 128
 #endif
 #ifndef QFS_BUDGET5
-#define QFS_BUDGET5 6400
+#define QFS_BUDGET5 6000
 #endif
 #ifndef QFS_SLICE5
-#define QFS_SLICE5 16
+#define QFS_SLICE5 24
 #endif
 #ifndef QFS_NT13
 #define QFS_NT13 256
@@ -68,13 +68,13 @@ struct StagedCfg {
 #define QFS_NT11 256
 #endif
 #ifndef QFS_SLICE7
-#define QFS_SLICE7 8
+#define QFS_SLICE7 12
 #endif
 #ifndef QFS_SLICE11
 #define QFS_SLICE11 8
 #endif
 #ifndef QFS_BUDGET7
-#define QFS_BUDGET7 8000
+#define QFS_BUDGET7 8400
 #endif
 #ifndef QFS_BUDGET11
 #define QFS_BUDGET11 16384
