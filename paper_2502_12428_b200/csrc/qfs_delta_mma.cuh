@@ -71,7 +71,7 @@ struct DeltaPiece {
 #define QFS_DMMA_RG5 5
 #endif
 #ifndef QFS_DMMA_SBW5
-#define QFS_DMMA_SBW5 6144
+#define QFS_DMMA_SBW5 6912   // fewer, larger phases; 54.3 KB per CTA still leaves four CTAs per SM (6144: 1.61, 6656 ... 7160: 1.52 ms)
 #endif
 #ifndef QFS_DMMA_SBW7
 #define QFS_DMMA_SBW7 5600   // 57.3 KB per CTA: four CTAs per SM (6144 words are 48 bytes too many for that: 9.4 -> 8.3 ms)
