@@ -37,7 +37,7 @@
 // A quad's phases may be split over several CTAs (SPLIT parts of equal work) so that the few hundred surfaces of an F_11 / F_13
 // chunk still fill 148 SMs.
 //
-// Measured (B200, 100 000 seeded surfaces): F_5 3.25 -> 1.6 ms, F_7 16.0 -> 8.3 ms, F_11 (4000 surfaces) 8.5 -> 3.6 ms,
+// Measured (B200, 100 000 seeded surfaces): F_5 3.25 -> 1.5 ms, F_7 16.0 -> 8.3 ms, F_11 (4000 surfaces) 8.5 -> 3.5 ms,
 // F_13 (2000 surfaces) 41.9 -> 5.0 ms against the DP4A kernels (qfs_delta.cuh, qfs_delta_direct.cuh), bit-identical Delta.
 #pragma once
 #include <algorithm>
