@@ -52,10 +52,16 @@ struct PowerCfg {
     static constexpr int FED_WARPS = (P >= 11) ? 4 : 8;  // warps per CTA in k_fedder: FED_WARPS / FED_WPS surfaces per CTA
     static constexpr int FED_BUF = qround16(qc3(4 * J0 + 3));
     static constexpr int RB_DEG = 4 * P;                // row-base tables up to this degree
-    static constexpr int FULL_NT = 256;
+#ifndef QFS_POWER_NT5
+#define QFS_POWER_NT5 128
+#endif
+    static constexpr int FULL_NT = (P <= 5) ? QFS_POWER_NT5 : 256;   // F_5: 128 threads x 12 CTAs 0.59 ms, 256 x 8 0.64, 512 x 4 0.79; F_7: 256 is best
     // CTAs per SM k_power_full is compiled for: shared memory allows 7 (p = 5), 5 (p = 7), 1 (p >= 11); at p <= 5 the 35
     // multiplier coefficients otherwise sit in 55 registers and leave room for four CTAs only (F_5: 0.555 -> 0.49 ms)
-    static constexpr int FULL_MINB = (P <= 5) ? 8 : (P == 7 ? 5 : 1);
+#ifndef QFS_POWER_MINB5
+#define QFS_POWER_MINB5 12
+#endif
+    static constexpr int FULL_MINB = (P <= 5) ? QFS_POWER_MINB5 : (P == 7 ? 5 : 1);
     static constexpr int FULL_BUF = S::NE_pad;
     // row-base tables rb_d for d = 4, 8, ..., RB_DEG; table d starts at rb_offset(d)
     static QFS_HD constexpr int rb_offset(int d) { return qrb_offset(d); }
