@@ -412,6 +412,63 @@ def measure_matrix_free(device, seed, checked):
     return out
 
 
+def measure_lazy(device, seed, checked):
+    """surfaces/s of the lazy operator-matrix mode (qfs_heights_lazy: the cap row of the first step decides before Delta and M
+    are built) on resident inputs (CUDA events) and end to end through height_batch(method="lazy") with pinned host buffers;
+    F_5, F_7 at 100000 seeded quartics, F_11 at 4000 and 20000, F_13 at 2000; heights and iterations compared with the eager path's."""
+    import time
+    import torch
+    from paper_2502_12428_b200 import height_batch
+    from paper_2502_12428_b200.engine import get_engine
+    out = {"note": "the operator-matrix path with the loop's early exit (height.py:135-144) taken before the matrix is built: "
+                   "(M g)[cap] is one row of M = N entries of Delta, evaluated from the factorised Witt carry (csrc/qfs_caprow.cuh); "
+                   "Delta and M are built and streamed for the surfaces it leaves undecided only (built); same heights and "
+                   "iterations; the headline and the roofline stay on the eager path, which builds M for every hard surface like the reference"}
+    for p, batch in ((5, 100000), (7, 100000), (11, 4000), (11, 20000), (13, 2000)):
+        host = cached_block(p, batch, seed, 0)
+        dev = torch.from_numpy(host).to(f"cuda:{device}")
+        hs = torch.empty(batch, dtype=torch.int8, device=dev.device)
+        its = torch.empty(batch, dtype=torch.int8, device=dev.device)
+        eng = get_engine(p, device)
+        for _ in range(3):
+            eng.heights(dev, 10, out=(hs, its), lazy=True)
+        torch.cuda.synchronize(device)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        steps = 5
+        e0.record()
+        for _ in range(steps):
+            eng.heights(dev, 10, out=(hs, its), lazy=True)
+        e1.record()
+        torch.cuda.synchronize(device)
+        ms = e0.elapsed_time(e1) / steps
+        st = eng.stats()
+        h = hs.cpu().numpy()
+        entry = {"value": batch / (ms * 1e-3), "unit": "surfaces/s", "ms_per_step": ms, "batch": batch,
+                 "hard": int(st["hard"]), "built": int(st["built"]), "hard_per_s": float((h != 1).sum()) / (ms * 1e-3),
+                 "stage_ms_per_step": {k: v for k, v in st.items() if k.startswith("ms_")}}
+        # end to end: pinned host buffers in and out through the public entry
+        pin_c = torch.from_numpy(host).pin_memory()
+        pin_h = torch.empty(batch, dtype=torch.int8).pin_memory()
+        pin_i = torch.empty(batch, dtype=torch.int8).pin_memory()
+        for _ in range(2):
+            height_batch(p, pin_c.numpy(), 10, devices=[device], method="lazy", out=(pin_h.numpy(), pin_i.numpy()))
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            height_batch(p, pin_c.numpy(), 10, devices=[device], method="lazy", out=(pin_h.numpy(), pin_i.numpy()))
+        entry["e2e"] = {"value": batch * steps / (time.perf_counter() - t0), "unit": "surfaces/s", "h2d_bytes_per_step": 35 * batch,
+                        "d2h_bytes_per_step": 2 * batch, "through": "height_batch(method='lazy'), pinned host buffers, host clock around the calls"}
+        eager = None
+        if p in checked and checked[p]["heights"].shape[0] == batch:
+            eager = (checked[p]["heights"], checked[p]["iters"])
+        else:
+            eh, ei = eng.heights(dev, 10)
+            eager = (eh.cpu().numpy(), ei.cpu().numpy())
+        entry["equals_eager_matrix_path"] = bool(np.array_equal(h, eager[0]) and np.array_equal(its.cpu().numpy(), eager[1]) and
+                                                 np.array_equal(pin_h.numpy(), eager[0]) and np.array_equal(pin_i.numpy(), eager[1]))
+        out[f"F_{p}" + ("" if (p, batch) != (11, 20000) else "_20000")] = entry
+    return out
+
+
 def gpu_line(args, p, res, world, with_cpu):
     batch, steps = args.batch, res["steps"]
     peak, peak_src = measured_peaks()
@@ -542,6 +599,7 @@ def main():
         if rank == 0 and world == 1:
             line["also"]["matrix_free"] = measure_matrix_free(local, args.seed, {5: res, 7: res7})
             line["also"]["single_surface"] = measure_single_surface(local, {5: res, 7: res7})
+            line["also"]["lazy_matrix"] = measure_lazy(local, args.seed, {5: res, 7: res7})
     if rank == 0:
         print(json.dumps(line))
     if dist is not None:

@@ -71,6 +71,9 @@ typedef struct qfs_stats {
     double  ms_matrix;
     double  ms_matvec;
     double  ms_total;        /* first launch to last completion              */
+    int64_t built;           /* surfaces whose Delta and M were built: = hard for qfs_heights, the ones the cap row left
+                                undecided for qfs_heights_lazy, 0 for qfs_heights_free */
+    double  ms_caprow;       /* qfs_heights_lazy: f^(p-1) and the cap row of the first step for every hard surface */
 } qfs_stats;
 
 int qfs_version(void);
@@ -113,6 +116,18 @@ int qfs_get_stats(const qfs_ctx *ctx, qfs_stats *out);
  * this library is quoted on (that path builds and streams M, like the
  * reference's height_matrix); it exists to cross-check it and as a fast mode. */
 int qfs_heights_free(qfs_ctx *ctx, const uint8_t *coeffs, size_t B, int bound,
+                     int8_t *heights, int8_t *iters, void *stream);
+
+/* The same heights and iteration counts on the operator-matrix path, with the
+ * early exit of height.py:135-144 taken BEFORE the matrix is built where the first
+ * step already decides: (M g)[cap] is one row of M, i.e. N entries of Delta
+ * (M[cap, c] = Delta[(p^2-1) - c], mtsmatrix.py:249-281), which csrc/qfs_caprow.cuh
+ * evaluates from the factorised Witt carry and dots with g.  A fraction 1 - 1/p of
+ * the hard surfaces gets height 2 there; Delta and M are built, and the chain run,
+ * only for the rest (qfs_stats.built).  Same arguments and semantics as qfs_heights.
+ * Like qfs_heights_free it is NOT the path the roofline is quoted on: qfs_heights
+ * builds M for every hard surface, as the reference does. */
+int qfs_heights_lazy(qfs_ctx *ctx, const uint8_t *coeffs, size_t B, int bound,
                      int8_t *heights, int8_t *iters, void *stream);
 
 /* ---- stage taps (parity against the reference's intermediates) ----------

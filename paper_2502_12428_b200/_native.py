@@ -19,7 +19,7 @@ QFS_OK, QFS_EINVAL, QFS_ECUDA, QFS_EINVARIANT, QFS_ENOMEM = 0, -1, -2, -3, -4
 
 EXPORTS = (
     "qfs_version", "qfs_get_shape", "qfs_create", "qfs_destroy", "qfs_last_error",
-    "qfs_set_workspace_limit", "qfs_set_chunk", "qfs_heights", "qfs_heights_free", "qfs_get_stats",
+    "qfs_set_workspace_limit", "qfs_set_chunk", "qfs_heights", "qfs_heights_free", "qfs_heights_lazy", "qfs_get_stats",
     "qfs_stage_power", "qfs_stage_delta", "qfs_stage_matrix", "qfs_stage_matvec_chain",
     "qfs_export_matrix", "qfs_debug_fill_workspaces", "qfs_cubic_heights", "qfs_sample_quartics", "qfs_form_heights",
     "qfs_literal_heights", "qfs_debug_occupancy",
@@ -35,7 +35,8 @@ class QfsStats(ctypes.Structure):
     _fields_ = [("surfaces", ctypes.c_int64), ("hard", ctypes.c_int64), ("matvec_steps", ctypes.c_int64),
                 ("kernel_launches", ctypes.c_int64), ("chunks", ctypes.c_int64), ("chunk_capacity", ctypes.c_int64),
                 ("ms_power", ctypes.c_double), ("ms_delta", ctypes.c_double), ("ms_matrix", ctypes.c_double),
-                ("ms_matvec", ctypes.c_double), ("ms_total", ctypes.c_double)]
+                ("ms_matvec", ctypes.c_double), ("ms_total", ctypes.c_double), ("built", ctypes.c_int64),
+                ("ms_caprow", ctypes.c_double)]
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}
@@ -84,6 +85,7 @@ def load():
     lib.qfs_set_chunk.argtypes = [vp, sz]
     lib.qfs_heights.argtypes = [vp, u8p, sz, ctypes.c_int, i8p, i8p, vp]
     lib.qfs_heights_free.argtypes = [vp, u8p, sz, ctypes.c_int, i8p, i8p, vp]
+    lib.qfs_heights_lazy.argtypes = [vp, u8p, sz, ctypes.c_int, i8p, i8p, vp]
     lib.qfs_get_stats.argtypes = [vp, ctypes.POINTER(QfsStats)]
     lib.qfs_stage_power.argtypes = [vp, u8p, sz, u8p, u8p]
     lib.qfs_stage_delta.argtypes = [vp, u8p, sz, u8p]

@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "../../include/qfs.h"
+#include "qfs_caprow.cuh"
 #include "qfs_chain.cuh"
 #include "qfs_cubic.cuh"
 #include "qfs_delta.cuh"
@@ -332,6 +333,7 @@ int build_tables(qfs_ctx* ctx)
         CU(cudaFuncSetAttribute(k_delta<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, DeltaCfg<P>::SMEM));
     CU(cudaFuncSetAttribute(k_delta_direct<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, DeltaDirectCfg<P>::SMEM));
     CU(cudaFuncSetAttribute(k_free<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, FreeCfg<P>::SMEM));
+    CU(cudaFuncSetAttribute(k_caprow<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, CapRowCfg<P>::SMEM));
     ctx->delta_direct = getenv("QFS_DELTA_DIRECT") ? 1 : 0;
     if (const char* e = getenv("QFS_DELTA_V")) ctx->delta_version = atoi(e);
     {   // phase plan of the tensor-core Witt carry (qfs_delta_mma.cuh)
@@ -604,9 +606,10 @@ float elapsed(cudaEvent_t a, cudaEvent_t b)
 
 // ---- the pipeline ----------------------------------------------------------------------------
 template <int P>
-int run_heights(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, int bound, int8_t* heights, int8_t* iters, void* user_stream, int matrix_free)
+int run_heights(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, int bound, int8_t* heights, int8_t* iters, void* user_stream, int mode)
 {
     using S = Shape<P>;
+    const bool matrix_free = mode == 1, lazy = mode == 2;   // 0: Delta and M for every hard surface (the reference's height_matrix)
     ctx->stats = qfs_stats{};
     ctx->stats.surfaces = (int64_t)B;
     if (B == 0) return QFS_OK;
@@ -660,6 +663,41 @@ int run_heights(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, int bound, int8_t
     }
     ctx->stats.ms_power += elapsed(ctx->ev[0], ctx->ev[1]);
     ctx->stats.hard = hard;
+    ctx->stats.built = matrix_free ? 0 : hard;
+
+    if (lazy && hard > 0) {
+        // Lazy mode (qfs_caprow.cuh): the cap row of the first operator application decides 1 - 1/p of the hard surfaces
+        // (height 2) from g, h, A, E alone; only the rest is compacted again and goes on to Delta, M and the chain.
+        const size_t perf = (size_t)(3 * S::pitch + S::Nh_pad + S::NE_pad);
+        const size_t capf = std::min<size_t>((size_t)hard, std::max<size_t>(1, ((size_t)1 << 30) / perf));
+        int rc = reserve_chunk_free<P>(ctx, capf);
+        if (rc) return rc;
+        CU(cudaEventRecord(ctx->ev[2], ctx->stream));
+        for (size_t done = 0; done < (size_t)hard; done += capf) {
+            const int cnt = (int)std::min<size_t>(capf, (size_t)hard - done);
+            if ((rc = launch_power_full<P>(ctx, d_coeffs, ctx->list.as<uint32_t>() + done, cnt, nullptr))) return rc;
+            k_caprow<P><<<cnt, CapRowCfg<P>::NT, CapRowCfg<P>::SMEM, ctx->stream>>>(
+                ctx->g.as<uint8_t>(), ctx->h.as<uint8_t>(), ctx->A.as<uint8_t>(), ctx->E.as<uint8_t>(),
+                ctx->unrank.as<uint32_t>() + qunrank_offset(P - 1), ctx->list.as<uint32_t>() + done, cnt, bound - 1, d_heights, d_iters);
+            ctx->stats.kernel_launches++;
+            CU(cudaGetLastError());
+        }
+        CU(cudaEventRecord(ctx->ev[3], ctx->stream));
+        k_compact<<<1, 1024, 0, ctx->stream>>>(d_heights, (int)B, ctx->list.as<uint32_t>(), d_flags + 2);
+        ctx->stats.kernel_launches++;
+        CU(cudaGetLastError());
+        rc = check_device_flags(ctx);
+        if (rc) return rc;
+        hard = ctx->h_flags[2];   // still pending: v1[cap] = 0 and bound > 2
+        ctx->stats.ms_caprow = elapsed(ctx->ev[2], ctx->ev[3]);
+        ctx->stats.built = hard;
+        if (hard == 0) {   // every hard surface was decided by the cap row: the chunk loop below (and its sum of iterations) is skipped
+            k_sum_iters<<<(unsigned)std::min<size_t>((B + 1023) / 1024, 1024), 1024, 0, ctx->stream>>>(d_iters, B, d_flags + 3);
+            ctx->stats.kernel_launches++;
+            if ((rc = check_device_flags(ctx))) return rc;
+            ctx->stats.matvec_steps = ctx->h_flags[3];
+        }
+    }
 
     if (hard > 0) {
         // chunk capacity from the workspace budget
@@ -1056,6 +1094,14 @@ int qfs_heights_free(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, int bound, i
     if (B && (!coeffs || !heights || !iters)) return fail(ctx, QFS_EINVAL, "NULL buffer");
     if (bound < 1 || bound > 127) return fail(ctx, QFS_EINVAL, "bound must be in 1..127, got %d", bound);
     QFS_FOR_PRIME(ctx->p, run_heights, ctx, coeffs, B, bound, heights, iters, stream, 1)
+}
+
+int qfs_heights_lazy(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, int bound, int8_t* heights, int8_t* iters, void* stream)
+{
+    if (!ctx) return QFS_EINVAL;
+    if (B && (!coeffs || !heights || !iters)) return fail(ctx, QFS_EINVAL, "NULL buffer");
+    if (bound < 1 || bound > 127) return fail(ctx, QFS_EINVAL, "bound must be in 1..127, got %d", bound);
+    QFS_FOR_PRIME(ctx->p, run_heights, ctx, coeffs, B, bound, heights, iters, stream, 2)
 }
 
 int qfs_stage_power(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, uint8_t* g, uint8_t* fedder)

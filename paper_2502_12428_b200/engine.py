@@ -93,12 +93,16 @@ class Engine:
         return st.as_dict()
 
     # -- hot path ----------------------------------------------------------------------------
-    def heights(self, coeffs, bound=10, out=None, matrix_free=False):
+    def heights(self, coeffs, bound=10, out=None, matrix_free=False, lazy=False):
         """(heights int8[B], iterations int8[B]); heights use 0 for infinity.
 
         coeffs: [B,35] uint8 numpy array or torch CUDA tensor.  With torch input the outputs are
         torch int8 tensors on the same device unless `out=(heights, iters)` is given.
+        matrix_free: the polynomial iteration (qfs_heights_free).  lazy: the operator-matrix path with the cap row of the
+        first step evaluated before Delta and M are built (qfs_heights_lazy); same results either way.
         """
+        if matrix_free and lazy:
+            raise DomainError("matrix_free and lazy are different modes: choose one")
         if not isinstance(bound, (int, np.integer)) or bound < 1:
             raise DomainError(f"bound must be a positive integer, got {bound}")
         B = int(coeffs.shape[0]) if hasattr(coeffs, "shape") and len(coeffs.shape) == 2 else -1
@@ -124,7 +128,7 @@ class Engine:
             import torch
             # the library orders its own stream behind this one (a NULL handle -- the default stream -- included)
             stream = torch.cuda.current_stream(coeffs.device).cuda_stream
-        fn = self.lib.qfs_heights_free if matrix_free else self.lib.qfs_heights
+        fn = self.lib.qfs_heights_free if matrix_free else (self.lib.qfs_heights_lazy if lazy else self.lib.qfs_heights)
         self._call(fn, cptr, B, int(bound), hp, ip, stream)
         del keep
         return hs, its

@@ -168,12 +168,16 @@ def height_batch(p: int, coeffs, bound: int = 10, devices=None, method: str = "m
     method: "matrix" (default; builds and streams the operator matrix like the reference's height_matrix) or
     "naive" (the polynomial iteration without the matrix, qfs_heights_free: the on-device counterpart of the
     reference's height_naive cross-check; same heights and iteration counts), or "literal" (p <= 7: the
-    reference's definitions executed literally on the device, csrc/qfs_literal.cuh -- the independent cross-check).
+    reference's definitions executed literally on the device, csrc/qfs_literal.cuh -- the independent cross-check),
+    or "lazy" (the matrix path with the loop's early exit taken before the matrix is built: the cap row of the first
+    step, N entries of Delta, decides 1 - 1/p of the hard surfaces; Delta and M are built for the rest only,
+    qfs_heights_lazy; same heights and iteration counts).
     out: optional pair of int8[B] numpy arrays to receive the results (e.g. pinned host memory).
     """
-    if method not in ("matrix", "naive", "literal"):
-        raise DomainError(f"unknown method {method!r}, expected 'matrix', 'naive' or 'literal'")
+    if method not in ("matrix", "naive", "literal", "lazy"):
+        raise DomainError(f"unknown method {method!r}, expected 'matrix', 'naive', 'literal' or 'lazy'")
     free = method == "naive"
+    lazy = method == "lazy"
     from .engine import get_engine
     c = _check_batch(p, coeffs, bound)
     B = c.shape[0]
@@ -200,14 +204,14 @@ def height_batch(p: int, coeffs, bound: int = 10, devices=None, method: str = "m
         return heights, iters
     blocks = split_blocks(B, len(devs))
     if len(blocks) == 1:
-        get_engine(p, devs[0]).heights(c, int(bound), out=(heights, iters), matrix_free=free)
+        get_engine(p, devs[0]).heights(c, int(bound), out=(heights, iters), matrix_free=free, lazy=lazy)
         return heights, iters
     errors = []
 
     def work(dev, start, cnt):
         try:
             get_engine(p, dev).heights(c[start:start + cnt], int(bound),
-                                       out=(heights[start:start + cnt], iters[start:start + cnt]), matrix_free=free)
+                                       out=(heights[start:start + cnt], iters[start:start + cnt]), matrix_free=free, lazy=lazy)
         except Exception as exc:  # re-raised on the caller's thread
             errors.append(exc)
 

@@ -191,8 +191,8 @@ def device_block(p: int, count: int, seed: int, worker: int, device: int = 0, bo
     if not is_prime(p):
         raise DomainError(f"p={p} is not prime")
     _check_engine_shape(p)
-    if method not in ("matrix", "naive"):
-        raise DomainError(f"unknown method {method!r}, expected 'matrix' or 'naive'")
+    if method not in ("matrix", "naive", "lazy"):
+        raise DomainError(f"unknown method {method!r}, expected 'matrix', 'naive' or 'lazy'")
     eng = get_engine(p, device)
     try:
         import torch   # only to own the device buffer of the block
@@ -200,15 +200,15 @@ def device_block(p: int, count: int, seed: int, worker: int, device: int = 0, bo
         host, clean = eng.sample(seed, worker, count)          # still drawn on the device, returned to the host
         if not clean:
             host = sample_block(p, count, seed, worker)
-        codes, iters = eng.heights(host, int(bound), matrix_free=(method == "naive"))
+        codes, iters = eng.heights(host, int(bound), matrix_free=(method == "naive"), lazy=(method == "lazy"))
         return host, codes, iters
     dev = torch.empty((count, NCOEFF), dtype=torch.uint8, device=f"cuda:{device}")
     _, clean = eng.sample(seed, worker, count, out=dev)
     if not clean:
         host = sample_block(p, count, seed, worker)
-        codes, iters = eng.heights(host, int(bound), matrix_free=(method == "naive"))
+        codes, iters = eng.heights(host, int(bound), matrix_free=(method == "naive"), lazy=(method == "lazy"))
         return host, codes, iters
-    hs, its = eng.heights(dev, int(bound), matrix_free=(method == "naive"))
+    hs, its = eng.heights(dev, int(bound), matrix_free=(method == "naive"), lazy=(method == "lazy"))
     return dev, hs.cpu().numpy(), its.cpu().numpy()
 
 
@@ -287,7 +287,8 @@ def spectrum_search(p: int, block: int = 100000, rng_seed: int = 0, bound: int =
     does not depend on the number of devices and the host does no per-sample work.
     Returns (witnesses {height code: (block, index, Quartic)}, HeightHistogram, blocks_done); height code
     0 = infinity.  `progress(blocks_done, hist, witnesses)` is called after every retired block.
-    `method` = "matrix" (operator matrix built and streamed) or "naive" (matrix-free iteration); same heights.
+    `method` = "matrix" (operator matrix built and streamed), "lazy" (the same, built only where the cap row of the first
+    step does not decide) or "naive" (matrix-free iteration); same heights.
     """
     devs = [0] if devices is None else [int(d) for d in devices]
     want = set(range(0, bound + 1)) if want is None else {0 if (isinstance(h, float) and math.isinf(h)) else int(h) for h in want}
@@ -422,7 +423,7 @@ def verify_fixtures(text: str, n: int = 4, primes=None, jobs: int = 1, method: s
     literally (csrc/qfs_literal.cuh, rows with p <= 7 only).
     `jobs` is ignored (one batched call replaces the reference's process pool).
     """
-    if method not in ("matrix", "naive", "literal"):
+    if method not in ("matrix", "naive", "literal", "lazy"):
         raise DomainError(f"unknown method {method!r}")
     rows = parse_fixtures(text, n)
     if primes is not None:
