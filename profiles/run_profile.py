@@ -15,11 +15,12 @@ ap.add_argument("--p", type=int, default=5)
 ap.add_argument("--batch", type=int, default=20000)
 ap.add_argument("--calls", type=int, default=2)
 ap.add_argument("--chunk", type=int, default=0)
+ap.add_argument("--lazy", action="store_true", help="qfs_heights_lazy (k_caprow before Delta and M)")
 a = ap.parse_args()
 c = bench.cached_block(a.p, 100000, 0, 0)[: a.batch]
 eng = get_engine(a.p, 0)
 if a.chunk:
     eng.set_chunk(a.chunk)
 for _ in range(a.calls):
-    hs, its = eng.heights(c, 10)
+    hs, its = eng.heights(c, 10, lazy=a.lazy)
     print(eng.stats())

@@ -23,6 +23,8 @@ for p in primes:
     m = eng.export_matrix(c[:2])
     hf, itf = eng.heights(c, 10, matrix_free=True)
     assert np.array_equal(hs, hf) and np.array_equal(its, itf)
+    hl, itl = eng.heights(c, 10, lazy=True)   # k_caprow + the second compaction (qfs_caprow.cuh)
+    assert np.array_equal(hs, hl) and np.array_equal(its, itl)
     if p <= 7:   # the literal route (qfs_literal.cuh)
         k = {3: 200, 5: 40, 7: 3}[p]
         lh, li, lg, ld = q.literal_heights(p, c[:k], 10, want_g=True, want_delta=True)

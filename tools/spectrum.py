@@ -24,7 +24,7 @@ def main():
     ap.add_argument("--max-blocks", type=int, default=100)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--devices", default="0")
-    ap.add_argument("--method", choices=("matrix", "naive"), default="matrix",
+    ap.add_argument("--method", choices=("matrix", "naive", "lazy"), default="matrix",
                     help="matrix: operator matrix in HBM + matvec chain (contract path); naive: matrix-free iteration")
     ap.add_argument("--want", default=None, help="comma-separated heights to look for (inf allowed); default 1..10,inf")
     ap.add_argument("--out", default=None)
