@@ -12,7 +12,11 @@
 // "lazy" mode of qfs_lib.cu (qfs_heights_lazy): same heights and iteration counts as qfs_heights, M built for ~1/p of the hard
 // surfaces only.
 //
-// One CTA per surface: h and the negated E in shared memory, a thread per column c, rowbase tables for the two index maps.
+// One CTA per surface.  The row only meets the points s with s_i in [p-4, p-1] (I_i = p^2-1-c_i, 0 <= c_i <= 4p-4): at most 64.
+// So the CTA first builds, in shared memory, the packed operands of qfs_delta_direct.cuh for exactly what the row needs -- per
+// residue class rho the 35 negated coefficients -E[rho + p t] (a pass over E: every entry belongs to one (class, tap)), per point s the 35 neighbours
+// h[s - t], both as 9 words of four bytes in the tap order of basis(4) -- and then a thread per column c turns its entry into
+// nine LDS pairs + DP4A, one exact reduction mod p and one multiply-add with g[c].
 #pragma once
 #include "qfs_shape.cuh"
 
@@ -20,44 +24,60 @@ template <int P>
 struct CapRowCfg {
     using S = Shape<P>;
     static constexpr int NT = (P >= 11) ? 256 : 128;
-    static constexpr int TE = S::dE + 1;    // rowbase table of E: [J1][J2]
-    static constexpr int TH = S::dh + 1;    // rowbase table of h: [u1][u2]
-    static constexpr int SMEM = S::Nh_pad + S::NE_pad + 4 * (TE * TE + TH * TH);
+    static constexpr int NWORD = 9;                   // 35 taps, four per word
+    static constexpr int NCLS = P * P * P;
+    static constexpr int S0 = (P > 4) ? P - 4 : 0;    // smallest s_i of the row
+    static constexpr int NPT = 64;                    // points (s1, s2, s3), s_i = S0 .. S0 + 3
+    static constexpr int SMEM = 4 * NWORD * (NCLS + NPT);
 };
 
 template <int P>
 __global__ void __launch_bounds__(CapRowCfg<P>::NT)
 k_caprow(const uint8_t* __restrict__ g_all, const uint8_t* __restrict__ h_all, const uint8_t* __restrict__ A_all,
-         const uint8_t* __restrict__ E_all, const uint32_t* __restrict__ unrank_d, const uint32_t* __restrict__ list, int count,
-         int max_steps, int8_t* __restrict__ heights, int8_t* __restrict__ iters)
+         const uint8_t* __restrict__ E_all, const uint32_t* __restrict__ unrank4, const uint32_t* __restrict__ unrank_E, const uint32_t* __restrict__ unrank_d,
+         const uint32_t* __restrict__ list, int count, int max_steps, int8_t* __restrict__ heights, int8_t* __restrict__ iters)
 {
     using S = Shape<P>;
     using C = CapRowCfg<P>;
-    extern __shared__ __align__(16) uint8_t cr_smem[];
-    uint8_t* sh = cr_smem;
-    uint8_t* sE = cr_smem + S::Nh_pad;
-    int* tE = reinterpret_cast<int*>(cr_smem + S::Nh_pad + S::NE_pad);
-    int* tH = tE + C::TE * C::TE;
+    extern __shared__ __align__(16) uint32_t cr_smem[];
+    uint32_t* sEc = cr_smem;                      // [class][9]: byte j = -E[rho + p t_j] mod p
+    uint32_t* sHp = cr_smem + C::NWORD * C::NCLS; // [point][9]: byte j = h[s - t_j]
     __shared__ uint32_t s_red[C::NT / 32];
+    __shared__ uint8_t s_rb4[25];                              // rank of the tap t in basis(4): rowbase(4, t1, t2) (+ t3)
+    __shared__ uint16_t s_rbh[(S::dh + 1) * (S::dh + 1)];      // rowbase(dh, u1, u2)
     const int slot = blockIdx.x, tid = threadIdx.x;
     if (slot >= count) return;
     const uint8_t* gg = g_all + (size_t)slot * S::pitch;
     const uint8_t* gA = A_all + (size_t)slot * S::pitch;
+    const uint8_t* gh = h_all + (size_t)slot * S::Nh_pad;
+    const uint8_t* gE = E_all + (size_t)slot * S::NE_pad;
     {
-        const uint4* src = reinterpret_cast<const uint4*>(h_all + (size_t)slot * S::Nh_pad);
-        for (int i = tid; i < S::Nh_pad / 16; i += C::NT) reinterpret_cast<uint4*>(sh)[i] = src[i];
-        const uint8_t* gE = E_all + (size_t)slot * S::NE_pad;
-        for (int i = tid; i < S::NE; i += C::NT) {
-            const uint32_t e = gE[i];
-            sE[i] = (uint8_t)(e ? P - e : 0u);   // -E mod p
+        // class table: every entry E[J] of the surface goes to exactly one (class, tap) = (J mod p, J div p); the rest stays zero
+        for (int i = tid; i < C::NWORD * (C::NCLS + C::NPT); i += C::NT) cr_smem[i] = 0u;
+        if (tid < 25) s_rb4[tid] = (uint8_t)((tid / 5 + tid % 5 <= 4) ? qrowbase(4, tid / 5, tid % 5) : 0);
+        for (int i = tid; i < (S::dh + 1) * (S::dh + 1); i += C::NT) {
+            const int a = i / (S::dh + 1), b = i - a * (S::dh + 1);
+            s_rbh[i] = (uint16_t)((a + b <= S::dh) ? qrowbase(S::dh, a, b) : 0);
         }
-        for (int i = tid; i < C::TE * C::TE; i += C::NT) {
-            const int a = i / C::TE, b = i - a * C::TE;
-            tE[i] = (a + b <= S::dE) ? qrowbase(S::dE, a, b) : -1;
+        __syncthreads();
+        uint8_t* bE = reinterpret_cast<uint8_t*>(sEc);
+        for (int e = tid; e < S::NE; e += C::NT) {
+            const uint32_t ev = gE[e];
+            if (ev == 0) continue;
+            const uint32_t m = unrank_E[e];
+            const int J1 = m & 255, J2 = (m >> 8) & 255, J3 = m >> 16;
+            const int t1 = J1 / P, t2 = J2 / P, t3 = J3 / P;
+            const int cls = ((J1 - P * t1) * P + (J2 - P * t2)) * P + (J3 - P * t3);
+            bE[cls * (4 * C::NWORD) + s_rb4[t1 * 5 + t2] + t3] = (uint8_t)(P - ev);   // |t| <= 4 because |J| <= 4p
         }
-        for (int i = tid; i < C::TH * C::TH; i += C::NT) {
-            const int a = i / C::TH, b = i - a * C::TH;
-            tH[i] = (a + b <= S::dh) ? qrowbase(S::dh, a, b) : -1;
+        // point table: h[s - t_j] for the 64 points the row can meet
+        uint8_t* bH = reinterpret_cast<uint8_t*>(sHp);
+        for (int e = tid; e < 35 * C::NPT; e += C::NT) {
+            const int pt = e / 35, j = e - pt * 35;
+            const uint32_t t = unrank4[j];
+            const int u1 = C::S0 + (pt >> 4) - (int)(t & 255), u2 = C::S0 + ((pt >> 2) & 3) - (int)((t >> 8) & 255),
+                      u3 = C::S0 + (pt & 3) - (int)(t >> 16);
+            if (u1 >= 0 && u2 >= 0 && u3 >= 0 && u1 + u2 + u3 <= S::dh) bH[pt * (4 * C::NWORD) + j] = gh[s_rbh[u1 * (S::dh + 1) + u2] + u3];
         }
     }
     __syncthreads();
@@ -69,26 +89,12 @@ k_caprow(const uint8_t* __restrict__ g_all, const uint8_t* __restrict__ h_all, c
         const uint32_t m = unrank_d[c];   // column c = the monomial with first exponents (c1, c2, c3)
         const int I1 = P * P - 1 - (int)(m & 255), I2 = P * P - 1 - (int)((m >> 8) & 255), I3 = P * P - 1 - (int)(m >> 16);
         const int s1 = I1 / P, s2 = I2 / P, s3 = I3 / P;
-        const int r1 = I1 - P * s1, r2 = I2 - P * s2, r3 = I3 - P * s3;
-        uint32_t acc = (r1 | r2 | r3) ? 0u : (uint32_t)gA[qrowbase(S::d, s1, s2) + s3];
+        const int cls = ((I1 - P * s1) * P + (I2 - P * s2)) * P + (I3 - P * s3);
+        const uint32_t* ec = sEc + cls * C::NWORD;
+        const uint32_t* hp = sHp + (((s1 - C::S0) * 4 + (s2 - C::S0)) * 4 + (s3 - C::S0)) * C::NWORD;
+        uint32_t acc = cls ? 0u : (uint32_t)gA[qrowbase(S::d, s1, s2) + s3];
 #pragma unroll
-        for (int t1 = 0; t1 <= 4; ++t1) {
-            const int u1 = s1 - t1, J1 = r1 + P * t1;
-            if (u1 < 0) break;
-#pragma unroll
-            for (int t2 = 0; t2 <= 4 - t1; ++t2) {
-                const int u2 = s2 - t2, J2 = r2 + P * t2;
-                if (u2 < 0) break;
-                const int bE = (J1 + J2 <= S::dE) ? tE[J1 * C::TE + J2] : -1;
-                const int bH = (u1 + u2 <= S::dh) ? tH[u1 * C::TH + u2] : -1;
-                if (bE < 0 || bH < 0) continue;
-#pragma unroll
-                for (int t3 = 0; t3 <= 4 - t1 - t2; ++t3) {
-                    const int u3 = s3 - t3, J3 = r3 + P * t3;
-                    if (u3 >= 0 && u1 + u2 + u3 <= S::dh && J1 + J2 + J3 <= S::dE) acc += (uint32_t)sE[bE + J3] * (uint32_t)sh[bH + u3];
-                }
-            }
-        }
+        for (int w = 0; w < C::NWORD; ++w) acc = __dp4a(ec[w], hp[w], acc);
         dot += (acc % (uint32_t)P) * gv;   // < N (p-1)^2 < 2^31 in total
     }
     dot = __reduce_add_sync(0xffffffffu, dot);
