@@ -18,12 +18,12 @@ def rank_block(total: int, rank: int, world: int):
     return blocks[rank] if rank < len(blocks) else (total, 0)
 
 
-def heights_sharded(p: int, coeffs, bound: int = 10, device=None, group=None, compute=None):
+def heights_sharded(p: int, coeffs, bound: int = 10, device=None, group=None, compute=None, method: str = "matrix"):
     """Heights of the global batch `coeffs` [B,35] (same array on every rank), computed block-wise.
 
     Every rank returns the full (heights int8[B], iterations int8[B]).  `device`: CUDA device index of this
     rank (default: rank % device_count); `compute(p, coeffs, bound, device)` replaces the CUDA engine in
-    CPU tests.
+    CPU tests; `method` as in height_batch ("matrix", "lazy", "naive").
     """
     import torch
     import torch.distributed as dist
@@ -35,7 +35,7 @@ def heights_sharded(p: int, coeffs, bound: int = 10, device=None, group=None, co
     if compute is None:
         from .height import height_batch
         dev = device if device is not None else rank % max(1, torch.cuda.device_count())
-        hs, its = height_batch(p, c[start:start + count], bound, devices=[dev]) if count else (np.empty(0, np.int8),) * 2
+        hs, its = height_batch(p, c[start:start + count], bound, devices=[dev], method=method) if count else (np.empty(0, np.int8),) * 2
     else:
         hs, its = compute(p, c[start:start + count], bound, device) if count else (np.empty(0, np.int8),) * 2
     if world == 1:
