@@ -5,7 +5,10 @@ must agree on every height and every iteration count.  With --literal N the firs
 through the literal route (qfs_literal_heights: dense powers, checked division, splitting operator; none of the engine's
 identities), p <= 7.
 
-    python tools/crosscheck.py --p 5 --count 10000000 [--block 1000000] [--seed 1] [--literal 100000]
+    python tools/crosscheck.py --p 5 --count 10000000 [--block 1000000] [--seed 1] [--literal 100000] [--lazy]
+
+--lazy replaces the matrix-free arm by the lazy operator-matrix mode (qfs_heights_lazy: the cap row of the first step decides
+before Delta and M are built), again on every height and every iteration count.
 """
 import argparse
 import json
@@ -25,6 +28,7 @@ ap.add_argument("--count", type=int, default=10000000)
 ap.add_argument("--block", type=int, default=1000000)
 ap.add_argument("--seed", type=int, default=1)
 ap.add_argument("--literal", type=int, default=0, help="surfaces per block that also go through the literal route")
+ap.add_argument("--lazy", action="store_true", help="second arm = qfs_heights_lazy instead of qfs_heights_free")
 a = ap.parse_args()
 eng = get_engine(a.p, 0)
 hist = np.zeros(12, dtype=np.int64)
@@ -41,7 +45,7 @@ while done < a.count:
     if not clean:
         c = torch.from_numpy(q.sample_block(a.p, n, a.seed, w)).cuda()
     t0 = time.perf_counter(); hm, im = eng.heights(c, 10); torch.cuda.synchronize(); t1 = time.perf_counter()
-    hf, jf = eng.heights(c, 10, matrix_free=True); torch.cuda.synchronize(); t2 = time.perf_counter()
+    hf, jf = eng.heights(c, 10, matrix_free=not a.lazy, lazy=a.lazy); torch.cuda.synchronize(); t2 = time.perf_counter()
     t_m += t1 - t0; t_f += t2 - t1
     hm, im, hf, jf = (x.cpu().numpy() for x in (hm, im, hf, jf))
     mism += int((hm != hf).sum() + (im != jf).sum())
@@ -56,6 +60,6 @@ while done < a.count:
     done += n; w += 1
 print(json.dumps({"p": a.p, "surfaces": done, "seed": a.seed, "mismatches": mism,
                   "histogram": {("inf" if h == 0 else str(h)): int(v) for h, v in enumerate(hist) if v},
-                  "matrix_path_s": round(t_m, 2), "matrix_free_s": round(t_f, 2),
+                  "matrix_path_s": round(t_m, 2), ("lazy_matrix_s" if a.lazy else "matrix_free_s"): round(t_f, 2),
                   "literal": {"surfaces": lit_done, "mismatches": lit_mism, "s": round(t_l, 2)}}))
 sys.exit(1 if mism or lit_mism else 0)
