@@ -99,6 +99,8 @@ print("F_5", round(d["value"]), {k: round(v, 3) for k, v in d["stage_ms_per_step
 for k, a in d["also"].items():
     if k == "single_surface":
         print(k, {kk: (round(v["ms_per_call"], 3), round(v["cpu_oracle_ms"], 1)) for kk, v in a.items()})
+    elif k == "lazy_matrix":
+        print(k, {kk: (round(v["value"]), v["built"], v["hard"]) for kk, v in a.items() if kk != "note"})
     elif k != "matrix_free":
         print(k, round(a["value"]), {kk: round(v, 3) for kk, v in a["stage_ms_per_step"].items()}, "frac", round(a["roofline"]["frac"], 3), "e2e", round(a["e2e"]["value"]))
     else:
