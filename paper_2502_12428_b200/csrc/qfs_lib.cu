@@ -716,7 +716,9 @@ int run_heights(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, int bound, int8_t
         // Lazy mode (qfs_caprow.cuh): the cap row of the first operator application decides 1 - 1/p of the hard surfaces
         // (height 2) from g, h, A, E alone; only the rest is compacted again and goes on to Delta, M and the chain.
         const size_t perf = (size_t)(3 * S::pitch + S::Nh_pad + S::NE_pad);
-        const size_t capf = std::min<size_t>((size_t)hard, std::max<size_t>(1, ((size_t)1 << 30) / perf));
+        const size_t budgetf = ctx->workspace_limit ? std::min<size_t>(ctx->workspace_limit, (size_t)1 << 30) : (size_t)1 << 30;
+        const size_t capf = ctx->chunk_override ? std::min<size_t>((size_t)hard, ctx->chunk_override)
+                                                : std::min<size_t>((size_t)hard, std::max<size_t>(1, budgetf / perf));
         int rc = reserve_chunk_free<P>(ctx, capf);
         if (rc) return rc;
         CU(cudaEventRecord(ctx->ev[2], ctx->stream));

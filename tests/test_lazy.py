@@ -63,3 +63,21 @@ def test_lazy_mode_through_the_search_driver():
     a = search.device_block(7, 3000, 0, 2, 0, 10, "matrix")
     b = search.device_block(7, 3000, 0, 2, 0, 10, "lazy")
     assert np.array_equal(np.asarray(a[1]), np.asarray(b[1]))
+
+
+def test_lazy_mode_with_chunked_filter_and_chunked_pipeline():
+    """qfs_set_chunk cuts both the cap-row pass and the pipeline behind it into chunks of that many surfaces."""
+    import paper_2502_12428_b200 as q
+    from paper_2502_12428_b200.engine import get_engine
+    for p, count, chunk in ((5, 30000, 257), (7, 8000, 61), (11, 1200, 5)):
+        c = q.sample_block(p, count, 23, 1)
+        eng = get_engine(p, 0)
+        h0, i0 = eng.heights(c, 10)
+        eng.set_chunk(chunk)
+        try:
+            h1, i1 = eng.heights(c, 10, lazy=True)
+            st = eng.stats()
+        finally:
+            eng.set_chunk(0)
+        assert np.array_equal(h0, h1) and np.array_equal(i0, i1), p
+        assert st["chunks"] == -(-st["built"] // ((chunk + 3) // 4 * 4)) or st["chunks"] == -(-st["built"] // chunk), (p, st)
