@@ -35,7 +35,8 @@ template <int P>
 __global__ void __launch_bounds__(CapRowCfg<P>::NT)
 k_caprow(const uint8_t* __restrict__ g_all, const uint8_t* __restrict__ h_all, const uint8_t* __restrict__ A_all,
          const uint8_t* __restrict__ E_all, const uint32_t* __restrict__ unrank4, const uint32_t* __restrict__ unrank_E, const uint32_t* __restrict__ unrank_d,
-         const uint32_t* __restrict__ list, int count, int max_steps, int8_t* __restrict__ heights, int8_t* __restrict__ iters)
+         const uint32_t* __restrict__ list, int count, int max_steps, int8_t* __restrict__ heights, int8_t* __restrict__ iters,
+         uint32_t* __restrict__ slotmap)
 {
     using S = Shape<P>;
     using C = CapRowCfg<P>;
@@ -105,10 +106,34 @@ k_caprow(const uint8_t* __restrict__ g_all, const uint8_t* __restrict__ h_all, c
 #pragma unroll
         for (int w = 0; w < C::NT / 32; ++w) tot += s_red[w];
         const bool decided = (tot % (uint32_t)P) != 0;
+        const uint32_t sid = list ? list[slot] : (uint32_t)slot;
         if (decided || max_steps <= 1) {   // max_steps = bound - 1 operator applications allowed: after one, an undecided surface is infinity
-            const uint32_t sid = list ? list[slot] : (uint32_t)slot;
             heights[sid] = (int8_t)(decided ? 2 : 0);
             iters[sid] = 1;
+        } else if (slotmap) {
+            slotmap[sid] = (uint32_t)slot;   // where the pending surface's g, h, A, E sit (k_gather_rows)
         }
+    }
+}
+
+// The surfaces the cap row left pending keep the g, h, A, E that k_power_full computed for the cap-row pass: slot k of the
+// compacted list takes the rows of the slot the surface had there (slotmap).  Rows are gathered into a scratch area (the rows
+// move towards lower slots, so an in-place copy would race) and copied back by the caller.
+struct GatherRows {
+    const uint8_t* src[4];
+    uint8_t* dst[4];
+    uint32_t row16[4];   // row sizes in 16-byte units
+};
+
+__global__ void __launch_bounds__(128) k_gather_rows(GatherRows gr, const uint32_t* __restrict__ list, const uint32_t* __restrict__ slotmap, int count)
+{
+    const int k = blockIdx.x;
+    if (k >= count) return;
+    const uint32_t j = slotmap[list[k]];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        const uint4* s = reinterpret_cast<const uint4*>(gr.src[a]) + (size_t)j * gr.row16[a];
+        uint4* d = reinterpret_cast<uint4*>(gr.dst[a]) + (size_t)k * gr.row16[a];
+        for (uint32_t i = threadIdx.x; i < gr.row16[a]; i += 128) d[i] = s[i];
     }
 }

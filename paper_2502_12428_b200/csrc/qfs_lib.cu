@@ -95,6 +95,7 @@ struct qfs_ctx {
     DevBuf unrank;                                  // per-p unrank tables for the power chain
     DevBuf coeffs, heights, iters, list;            // batch-sized
     DevBuf compact_counts;                          // pending surfaces per tile of the batch (launch_compact)
+    DevBuf slotmap;                                 // lazy mode: slot of a pending surface in the cap-row pass (k_gather_rows)
     DevBuf g, h, A, E, delta, M, v1;                // chunk-sized
     DevBuf chain_scratch;                           // 2 x pitch: the vector exchange of k_chain_grid
     DevBuf tapA, tapB;                              // staging for the stage taps
@@ -712,6 +713,7 @@ int run_heights(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, int bound, int8_t
     ctx->stats.hard = hard;
     ctx->stats.built = matrix_free ? 0 : hard;
 
+    bool rows_kept = false;
     if (lazy && hard > 0) {
         // Lazy mode (qfs_caprow.cuh): the cap row of the first operator application decides 1 - 1/p of the hard surfaces
         // (height 2) from g, h, A, E alone; only the rest is compacted again and goes on to Delta, M and the chain.
@@ -721,6 +723,9 @@ int run_heights(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, int bound, int8_t
                                                 : std::min<size_t>((size_t)hard, std::max<size_t>(1, budgetf / perf));
         int rc = reserve_chunk_free<P>(ctx, capf);
         if (rc) return rc;
+        // one pass over all hard surfaces: the pending ones keep their g, h, A, E for the pipeline (k_gather_rows below)
+        rows_kept = capf >= (size_t)hard && !getenv("QFS_LAZY_RECOMPUTE");
+        if (rows_kept) CU(ctx->slotmap.reserve(B * sizeof(uint32_t)));
         CU(cudaEventRecord(ctx->ev[2], ctx->stream));
         for (size_t done = 0; done < (size_t)hard; done += capf) {
             const int cnt = (int)std::min<size_t>(capf, (size_t)hard - done);
@@ -729,7 +734,7 @@ int run_heights(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, int bound, int8_t
                 ctx->g.as<uint8_t>(), ctx->h.as<uint8_t>(), ctx->A.as<uint8_t>(), ctx->E.as<uint8_t>(),
                 ctx->unrank.as<uint32_t>() + qunrank_offset(1), ctx->unrank.as<uint32_t>() + qunrank_offset(P),
                 ctx->unrank.as<uint32_t>() + qunrank_offset(P - 1),
-                ctx->list.as<uint32_t>() + done, cnt, bound - 1, d_heights, d_iters);
+                ctx->list.as<uint32_t>() + done, cnt, bound - 1, d_heights, d_iters, rows_kept ? ctx->slotmap.as<uint32_t>() : nullptr);
             ctx->stats.kernel_launches++;
             CU(cudaGetLastError());
         }
@@ -769,6 +774,7 @@ int run_heights(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, int bound, int8_t
             const size_t wave = (size_t)ctx->delta_wave;
             if (wave && cap >= wave && cap < 16 * wave) cap = cap / wave * wave;
         }
+        const void* kept[4] = {ctx->g.ptr, ctx->h.ptr, ctx->A.ptr, ctx->E.ptr};
         while (true) {
             int rc = matrix_free ? reserve_chunk_free<P>(ctx, cap) : reserve_chunk<P>(ctx, cap);
             if (rc == QFS_OK) break;
@@ -792,7 +798,26 @@ int run_heights(qfs_ctx* ctx, const uint8_t* coeffs, size_t B, int bound, int8_t
             cudaEvent_t* ev = &ctx->chunk_ev[5 * ci];
             int rc;
             CU(cudaEventRecord(ev[0], ctx->stream));
-            if ((rc = launch_power_full<P>(ctx, d_coeffs, d_list + done, cnt, nullptr))) return rc;
+            if (rows_kept && nchunks == 1 && kept[0] == ctx->g.ptr && kept[1] == ctx->h.ptr && kept[2] == ctx->A.ptr && kept[3] == ctx->E.ptr) {
+                // lazy mode, one chunk: g, h, A, E of the pending surfaces are still in the workspaces, at the slots of the cap-row
+                // pass; gather them to the slots of the compacted list through the (still unused) matrix workspace
+                GatherRows gr;
+                const uint8_t* src[4] = {ctx->g.as<uint8_t>(), ctx->h.as<uint8_t>(), ctx->A.as<uint8_t>(), ctx->E.as<uint8_t>()};
+                const size_t rowb[4] = {(size_t)S::pitch, (size_t)S::Nh_pad, (size_t)S::pitch, (size_t)S::NE_pad};
+                uint8_t* scratch = ctx->M.as<uint8_t>();
+                size_t off = 0;
+                for (int a = 0; a < 4; ++a) {
+                    gr.src[a] = src[a];
+                    gr.dst[a] = scratch + off;
+                    gr.row16[a] = (uint32_t)(rowb[a] / 16);
+                    off += (size_t)cnt * rowb[a];
+                }
+                k_gather_rows<<<cnt, 128, 0, ctx->stream>>>(gr, d_list, ctx->slotmap.as<uint32_t>(), cnt);
+                ctx->stats.kernel_launches++;
+                CU(cudaGetLastError());
+                for (int a = 0; a < 4; ++a)
+                    CU(cudaMemcpyAsync(const_cast<uint8_t*>(src[a]), gr.dst[a], (size_t)cnt * rowb[a], cudaMemcpyDeviceToDevice, ctx->stream));
+            } else if ((rc = launch_power_full<P>(ctx, d_coeffs, d_list + done, cnt, nullptr))) return rc;
             CU(cudaEventRecord(ev[1], ctx->stream));
             if (matrix_free) {
                 // the operator iteration without Delta and without M (qfs_free.cuh): stage times delta = matrix = 0

@@ -81,3 +81,25 @@ def test_lazy_mode_with_chunked_filter_and_chunked_pipeline():
             eng.set_chunk(0)
         assert np.array_equal(h0, h1) and np.array_equal(i0, i1), p
         assert st["chunks"] == -(-st["built"] // ((chunk + 3) // 4 * 4)) or st["chunks"] == -(-st["built"] // chunk), (p, st)
+
+
+def test_lazy_mode_kept_rows_equal_recomputed_rows_and_survive_poisoned_workspaces():
+    """One chunk: the pending surfaces keep the g, h, A, E of the cap-row pass (k_gather_rows); QFS_LAZY_RECOMPUTE=1 runs
+    k_power_full on them again instead.  Both must agree with the eager path, also on workspaces filled with garbage."""
+    import paper_2502_12428_b200 as q
+    from paper_2502_12428_b200.engine import get_engine
+    for p, count in ((3, 2001), (5, 20003), (7, 5002), (11, 801)):
+        c = q.sample_block(p, count, 29, 2)
+        eng = get_engine(p, 0)
+        h0, i0 = eng.heights(c, 10)
+        for byte in (0x00, 0xFF, 0x5A):
+            eng.debug_fill_workspaces(byte)
+            h1, i1 = eng.heights(c, 10, lazy=True)
+            assert np.array_equal(h0, h1) and np.array_equal(i0, i1), (p, byte)
+        os.environ["QFS_LAZY_RECOMPUTE"] = "1"
+        try:
+            eng.debug_fill_workspaces(0xA5)
+            h2, i2 = eng.heights(c, 10, lazy=True)
+        finally:
+            del os.environ["QFS_LAZY_RECOMPUTE"]
+        assert np.array_equal(h0, h2) and np.array_equal(i0, i2), p
