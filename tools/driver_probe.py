@@ -46,7 +46,7 @@ for w in range(3, 3 + nb):
     u = np.unique(codes)
     t = lap("unique", t)
 print(f"p={p} block={block}: per block ms " + " ".join(f"{k}={1e3 * v / nb:.3f}" for k, v in acc.items()))
-for method in ("matrix", "naive"):
+for method in ("matrix", "lazy", "naive"):
     t0 = time.perf_counter()
     wit, hist, nblk = search.spectrum_search(p, block=block, rng_seed=0, bound=10, max_blocks=30, want={99}, method=method)
     dt = time.perf_counter() - t0
