@@ -34,6 +34,35 @@ __device__ __forceinline__ uint4 ld_stream16(const uint4* p)
     return r;
 }
 
+// The loop only ever tests v[cap] (height.py:141-143), so the LAST operator application of a surface needs one row of M, not M:
+// before streaming the matrix for a step the CTA computes the cap row's dot product with the current vector; if it is nonzero the
+// height is decided and the other N - 1 rows of that step are never read.  A surface of height h reads M h - 3 times instead of
+// h - 2 (height 3, a fraction 1 - 1/p of what reaches the chain: not at all).  Not taken when a trace of the vectors is asked for.
+template <int P, int NT>
+__device__ __forceinline__ bool cap_row_hit(const uint8_t* __restrict__ M, const uint8_t* v, uint32_t* s_red)
+{
+    using S = Shape<P>;
+    constexpr int NCHR = (S::N + 15) / 16;
+    const uint4* mrow = reinterpret_cast<const uint4*>(M + (size_t)S::cap * S::pitch);
+    uint32_t acc = 0;
+    for (int ch = threadIdx.x; ch < NCHR; ch += NT) {
+        const uint4 m = ld_stream16(mrow + ch);
+        const uint4 x = reinterpret_cast<const uint4*>(v)[ch];
+        acc = __dp4a(m.x, x.x, acc);
+        acc = __dp4a(m.y, x.y, acc);
+        acc = __dp4a(m.z, x.z, acc);
+        acc = __dp4a(m.w, x.w, acc);
+    }
+    acc = __reduce_add_sync(0xffffffffu, acc);
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    uint32_t tot = 0;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) tot += s_red[w];   // <= N (p-1)^2 < 2^31
+    __syncthreads();
+    return tot % (uint32_t)P != 0;
+}
+
 template <int P>
 __global__ void __launch_bounds__(ChainCfg<P>::NT, ChainCfg<P>::CTAS_PER_SM)
 k_chain(const uint8_t* __restrict__ M_all, const uint8_t* __restrict__ v0_all, const uint32_t* __restrict__ list,
@@ -44,6 +73,7 @@ k_chain(const uint8_t* __restrict__ M_all, const uint8_t* __restrict__ v0_all, c
     using C = ChainCfg<P>;
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ int s_slot;
+    __shared__ uint32_t s_red[C::NT / 32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int NW = C::NT / 32;
     constexpr int NCH = S::pitch / 16;
@@ -86,6 +116,14 @@ k_chain(const uint8_t* __restrict__ M_all, const uint8_t* __restrict__ v0_all, c
         __syncthreads();
         int height = 0, it = start_it;
         for (int step = start_it + 1; step <= max_steps; ++step) {
+            if (!trace) {
+                const bool hit = cap_row_hit<P, C::NT>(M, va, s_red);
+                if (hit || step == max_steps) {   // decided, or the last step allowed: the rest of v_step is never used
+                    ++it;
+                    if (hit) height = step + 1;
+                    break;
+                }
+            }
             for (int row = warp * C::UNROLL; row < S::N; row += NW * C::UNROLL) {
                 uint32_t acc[C::UNROLL];
 #pragma unroll
@@ -168,6 +206,7 @@ k_chain_grid(const uint8_t* __restrict__ M_all, const uint8_t* __restrict__ v0_a
     extern __shared__ __align__(16) uint8_t smem[];
     uint8_t* sv = smem;                 // the current vector, pad bytes zero
     uint8_t* sflag = smem + S::pitch;   // v0[slot][cap] of every slot of the launch
+    __shared__ uint32_t s_red[C::NT / 32];
     const int tid = threadIdx.x, lane = tid & 31;
     // consecutive rows go to different CTAs: every SM streams the same number of rows (+-1)
     const int gw = (tid >> 5) * gridDim.x + blockIdx.x, GW = gridDim.x * (C::NT / 32);
@@ -205,6 +244,16 @@ k_chain_grid(const uint8_t* __restrict__ M_all, const uint8_t* __restrict__ v0_a
         __syncthreads();
         int height = 0, it = start_it;
         for (int step = start_it + 1; step <= max_steps; ++step) {
+            if (!trace) {
+                // every CTA holds the same vector and takes the same decision: no grid barrier for the test (and none is skipped
+                // in a way that matters: a half of the scratch is rewritten only after a barrier that follows its last read)
+                const bool hit = cap_row_hit<P, C::NT>(M, sv, s_red);
+                if (hit || step == max_steps) {
+                    ++it;
+                    if (hit) height = step + 1;
+                    break;
+                }
+            }
             uint8_t* nxt = scratch + (size_t)par * S::pitch;
             for (int row = gw; row < S::N; row += GW) {
                 const uint4* mrow = reinterpret_cast<const uint4*>(M + (size_t)row * S::pitch);
