@@ -409,3 +409,31 @@ def test_stage_kernels_keep_their_resident_cta_counts(p, want):
     got = (occ["k_power_full"], occ["k_delta_mma"], occ["k_matrix_staged"], occ["k_chain"])
     for name, g, w in zip(("k_power_full", "k_delta_mma", "k_matrix_staged", "k_chain"), got, want):
         assert w is None or g >= w, f"{name}<{p}>: {g} resident CTAs per SM, tuned for {w}"
+
+
+@pytest.mark.parametrize("p", [3, 5, 7])
+def test_chain_cap_row_test_equals_the_traced_chain(p, monkeypatch):
+    """Without a trace the chain kernels test the cap row of a step before they stream M for it (qfs_chain.cuh: cap_row_hit) and
+    skip the last application's other rows; with a trace they compute every vector.  Same heights and iteration counts from the
+    same matrices and start vectors, for both kernels, from v0 = g (start at step 1) and for every step budget."""
+    import paper_2502_12428_b200 as q
+    from paper_2502_12428_b200.engine import Engine
+    c = q.sample_block(p, {3: 400, 5: 300, 7: 120}[p], 37, 0)
+    for mode in ("0", "1"):
+        monkeypatch.setenv("QFS_CHAIN_GRID", mode)
+        eng = Engine(p, 0)
+        try:
+            g, fed = eng.stage_power(c)
+            hard = np.flatnonzero(fed == 0)[: {3: 60, 5: 40, 7: 12}[p]]
+            M = eng.export_matrix(c[hard]).astype(np.uint8)
+            want_h, want_i = eng.heights(c[hard], 10)
+            for steps in (1, 2, 3, 9):
+                h1, i1, tr = eng.stage_matvec_chain(M, g[hard], steps, trace=True)
+                h0, i0 = eng.stage_matvec_chain(M, g[hard], steps)
+                assert np.array_equal(h0, h1) and np.array_equal(i0, i1), (p, mode, steps)
+                for k in range(len(hard)):   # the traced vectors decide exactly as reported
+                    hit = [s for s in range(int(i1[k])) if tr[k][s][eng.shape.cap] != 0]
+                    assert (hit == [int(i1[k]) - 1] and int(h1[k]) == int(i1[k]) + 1) or (hit == [] and int(h1[k]) == 0 and int(i1[k]) == steps)
+            assert np.array_equal(h0, want_h) and np.array_equal(i0, want_i)
+        finally:
+            eng.close()
